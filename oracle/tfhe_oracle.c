@@ -1,0 +1,658 @@
+/*
+ * TEST INFRASTRUCTURE ONLY — see tfhe_oracle.h for scope and anchors.
+ *
+ * Compiled with -O2 -ffp-contract=off: every floating-point rounding below
+ * is the one written (fma() is a single rounding, a*b and a+b are one each),
+ * which is what makes the GPU comparison bit-exact.
+ *
+ * Algorithm anchors
+ *  - plaintext space and LUT semantics: Lut16 / negacyclic_eval
+ *    (proj/include/leuven/lut.hpp:9-24, proj/src/lut.cpp:9-16): values mod 32,
+ *    inputs in [16,32) return -entries[x-16] mod 32. The test polynomial
+ *    below realises exactly this, with Delta = 2^64/32.
+ *  - decrypt = nearest multiple of Delta (SimBackend::decrypt returns the
+ *    plaintext residue, proj/include/leuven/backend.hpp:93).
+ *  - KS_PBS pipeline, gadget decomposition, GGSW external product, sample
+ *    extract: TFHE-rs v0.7.2 published algorithm (not vendored; named in
+ *    PAPER.md:1236), restated here with our own operation order.
+ */
+#include "tfhe_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+#include <unistd.h>
+
+enum {
+  D_SK_SMALL = 1,
+  D_SK_GLWE = 2,
+  D_BSK_MASK = 3,
+  D_BSK_NOISE = 4,
+  D_KSK_MASK = 5,
+  D_KSK_NOISE = 6,
+  D_ENC_MASK = 7,
+  D_ENC_NOISE = 8,
+};
+
+struct orc_ctx {
+  orc_params p;
+  uint64_t seed;
+  uint8_t* sk_small;
+  uint8_t* sk_glwe;
+  uint64_t* ksk;
+  uint64_t* bsk;
+  double* bskf;    /* interleaved (re, im) */
+  double* tw;      /* W[t] = exp(-2 pi i t / M), t < M/2, interleaved */
+  double* twist;   /* zeta^j = exp(i pi j / N), j < M */
+  double* untwist; /* zeta^-j / M */
+  uint32_t M;      /* N/2 */
+  uint32_t logM;
+};
+
+/* ------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon et al., SC'11), the Random123 round function.  */
+
+static inline void mulhilo32(uint32_t a, uint32_t b, uint32_t* hi, uint32_t* lo) {
+  uint64_t p = (uint64_t)a * (uint64_t)b;
+  *hi = (uint32_t)(p >> 32);
+  *lo = (uint32_t)p;
+}
+
+void orc_philox(uint64_t seed, uint32_t domain, uint64_t idx, uint32_t out[4]) {
+  uint32_t c0 = (uint32_t)idx, c1 = (uint32_t)(idx >> 32), c2 = domain, c3 = 0;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint32_t hi0, lo0, hi1, lo1;
+    mulhilo32(0xD2511F53u, c0, &hi0, &lo0);
+    mulhilo32(0xCD9E8D57u, c2, &hi1, &lo1);
+    uint32_t n0 = hi1 ^ c1 ^ k0;
+    uint32_t n1 = lo1;
+    uint32_t n2 = hi0 ^ c3 ^ k1;
+    uint32_t n3 = lo0;
+    c0 = n0;
+    c1 = n1;
+    c2 = n2;
+    c3 = n3;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+uint64_t orc_rand_u64(uint64_t seed, uint32_t domain, uint64_t idx) {
+  uint32_t o[4];
+  orc_philox(seed, domain, idx, o);
+  return ((uint64_t)o[1] << 32) | o[0];
+}
+
+/* TUniform(b): integers in [-2^b, 2^b], endpoints at half weight. */
+int64_t orc_tuniform(uint64_t seed, uint32_t domain, uint64_t idx, uint32_t b) {
+  uint64_t x = orc_rand_u64(seed, domain, idx) & ((UINT64_C(1) << (b + 2)) - 1);
+  return (int64_t)(x >> 1) + (int64_t)(x & 1) - ((int64_t)1 << b);
+}
+
+orc_params orc_default_params(void) {
+  orc_params p;
+  p.n = 880;
+  p.N = 2048;
+  p.k = 1;
+  p.pbs_base_log = 23;
+  p.pbs_level = 1;
+  p.ks_base_log = 3;
+  p.ks_level = 5;
+  p.lwe_noise_log2 = 44;
+  p.glwe_noise_log2 = 17;
+  return p;
+}
+
+/* ------------------------------------------------------------------ */
+/* threading helper                                                     */
+
+typedef void (*range_fn)(void* arg, size_t lo, size_t hi);
+typedef struct {
+  range_fn fn;
+  void* arg;
+  size_t lo, hi;
+} range_job;
+
+static void* range_thread(void* a) {
+  range_job* j = (range_job*)a;
+  j->fn(j->arg, j->lo, j->hi);
+  return NULL;
+}
+
+static int resolve_threads(int threads) {
+  if (threads > 0) return threads;
+  long n = sysconf(_SC_NPROCESSORS_ONLN);
+  return n > 0 ? (int)n : 1;
+}
+
+static void parallel_for(size_t count, int threads, range_fn fn, void* arg) {
+  threads = resolve_threads(threads);
+  if ((size_t)threads > count) threads = (int)count;
+  if (threads <= 1) {
+    if (count) fn(arg, 0, count);
+    return;
+  }
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+  range_job* jobs = (range_job*)malloc(sizeof(range_job) * (size_t)threads);
+  for (int t = 0; t < threads; ++t) {
+    jobs[t].fn = fn;
+    jobs[t].arg = arg;
+    jobs[t].lo = count * (size_t)t / (size_t)threads;
+    jobs[t].hi = count * (size_t)(t + 1) / (size_t)threads;
+    pthread_create(&th[t], NULL, range_thread, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+  free(th);
+  free(jobs);
+}
+
+/* ------------------------------------------------------------------ */
+/* polynomial helpers over Z_{2^64}[X]/(X^N+1)                         */
+
+/* out = X^e * in, e in [0, 2N) */
+static void poly_rotate(const uint64_t* in, uint64_t* out, uint32_t N, uint32_t e) {
+  for (uint32_t j = 0; j < N; ++j) {
+    uint32_t t = (j + 2 * N - e) % (2 * N);
+    out[j] = t < N ? in[t] : (uint64_t)0 - in[t - N];
+  }
+}
+
+/* acc += a * s (negacyclic), s binary */
+static void poly_mul_binary_acc(uint64_t* acc, const uint64_t* a, const uint8_t* s,
+                                uint32_t N) {
+  for (uint32_t t = 0; t < N; ++t) {
+    if (!s[t]) continue;
+    /* X^t * a */
+    for (uint32_t j = 0; j < N; ++j) {
+      if (j + t < N)
+        acc[j + t] += a[j];
+      else
+        acc[j + t - N] -= a[j];
+    }
+  }
+}
+
+/* acc += d * b (negacyclic), d small signed, exact mod 2^64 */
+static void poly_mul_small_acc(uint64_t* acc, const int64_t* d, const uint64_t* b,
+                               uint32_t N) {
+  for (uint32_t t = 0; t < N; ++t) {
+    uint64_t dt = (uint64_t)d[t];
+    if (!dt) continue;
+    for (uint32_t j = 0; j < N; ++j) {
+      uint64_t v = dt * b[j];
+      if (j + t < N)
+        acc[j + t] += v;
+      else
+        acc[j + t - N] -= v;
+    }
+  }
+}
+
+/* signed gadget decomposition, closest representable, digits in [-B/2, B/2),
+ * level index 0 = most significant (weight q/B). */
+static void decompose(uint64_t x, uint32_t base_log, uint32_t level, int64_t* digits) {
+  const uint32_t shift = 64 - base_log * level;
+  uint64_t v = (x + (UINT64_C(1) << (shift - 1))) >> shift;
+  const uint64_t mask = (UINT64_C(1) << base_log) - 1;
+  const int64_t half = (int64_t)1 << (base_log - 1);
+  for (int l = (int)level - 1; l >= 0; --l) {
+    int64_t d = (int64_t)(v & mask);
+    v >>= base_log;
+    if (d >= half) {
+      d -= (int64_t)1 << base_log;
+      v += 1;
+    }
+    digits[l] = d;
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* FFT specification                                                    */
+
+static inline void cmul(double ar, double ai, double br, double bi, double* r, double* i) {
+  double t1 = ai * bi;
+  double t2 = ai * br;
+  *r = fma(ar, br, -t1);
+  *i = fma(ar, bi, t2);
+}
+
+static void fft_dif(const orc_ctx* c, double* x /* interleaved M */) {
+  const uint32_t M = c->M;
+  for (uint32_t s = 0; s < c->logM; ++s) {
+    const uint32_t half = M >> (s + 1);
+    for (uint32_t blk = 0; blk < M; blk += 2 * half) {
+      for (uint32_t j = 0; j < half; ++j) {
+        double* u = x + 2 * (blk + j);
+        double* v = x + 2 * (blk + j + half);
+        const double* w = c->tw + 2 * ((size_t)j << s);
+        double sr = u[0] + v[0], si = u[1] + v[1];
+        double tr = u[0] - v[0], ti = u[1] - v[1];
+        u[0] = sr;
+        u[1] = si;
+        cmul(tr, ti, w[0], w[1], &v[0], &v[1]);
+      }
+    }
+  }
+}
+
+static void fft_dit_inverse(const orc_ctx* c, double* x) {
+  const uint32_t M = c->M;
+  for (int s = (int)c->logM - 1; s >= 0; --s) {
+    const uint32_t half = M >> (s + 1);
+    for (uint32_t blk = 0; blk < M; blk += 2 * half) {
+      for (uint32_t j = 0; j < half; ++j) {
+        double* p = x + 2 * (blk + j);
+        double* q = x + 2 * (blk + j + half);
+        const double* w = c->tw + 2 * ((size_t)j << s);
+        double qr, qi;
+        cmul(q[0], q[1], w[0], -w[1], &qr, &qi);
+        double pr = p[0], pi = p[1];
+        p[0] = pr + qr;
+        p[1] = pi + qi;
+        q[0] = pr - qr;
+        q[1] = pi - qi;
+      }
+    }
+  }
+}
+
+static inline uint64_t f64_to_torus(double y) {
+  const double two64 = 18446744073709551616.0;
+  const double inv64 = 5.42101086242752217e-20; /* 2^-64 */
+  double r = rint(y * inv64);
+  double d = y - r * two64;
+  if (d >= 9223372036854775808.0) d -= two64;
+  return (uint64_t)(int64_t)llrint(d);
+}
+
+static void forward_i64(const orc_ctx* c, const int64_t* a, double* out) {
+  const uint32_t M = c->M;
+  for (uint32_t j = 0; j < M; ++j) {
+    double re = (double)a[j], im = (double)a[j + M];
+    cmul(re, im, c->twist[2 * j], c->twist[2 * j + 1], &out[2 * j], &out[2 * j + 1]);
+  }
+  fft_dif(c, out);
+}
+
+static void backward_torus(const orc_ctx* c, double* spec /* destroyed */, uint64_t* out) {
+  const uint32_t M = c->M;
+  fft_dit_inverse(c, spec);
+  for (uint32_t j = 0; j < M; ++j) {
+    double re, im;
+    cmul(spec[2 * j], spec[2 * j + 1], c->untwist[2 * j], c->untwist[2 * j + 1], &re, &im);
+    out[j] = f64_to_torus(re);
+    out[j + M] = f64_to_torus(im);
+  }
+}
+
+void orc_fft_forward_i64(const orc_ctx* c, const int64_t* poly, double* spec) {
+  forward_i64(c, poly, spec);
+}
+
+void orc_fft_backward_torus(const orc_ctx* c, const double* spec, uint64_t* poly) {
+  double* tmp = (double*)malloc(sizeof(double) * 2 * c->M);
+  memcpy(tmp, spec, sizeof(double) * 2 * c->M);
+  backward_torus(c, tmp, poly);
+  free(tmp);
+}
+
+static void build_tables(orc_ctx* c) {
+  const uint32_t N = c->p.N, M = N / 2;
+  c->M = M;
+  c->logM = 0;
+  while ((1u << c->logM) < M) ++c->logM;
+  const long double PI = 3.141592653589793238462643383279502884L;
+  c->tw = (double*)malloc(sizeof(double) * M);
+  for (uint32_t t = 0; t < M / 2; ++t) {
+    long double ang = 2.0L * PI * (long double)t / (long double)M;
+    c->tw[2 * t] = (double)cosl(ang);
+    c->tw[2 * t + 1] = (double)(-sinl(ang));
+  }
+  c->twist = (double*)malloc(sizeof(double) * 2 * M);
+  c->untwist = (double*)malloc(sizeof(double) * 2 * M);
+  for (uint32_t j = 0; j < M; ++j) {
+    long double ang = PI * (long double)j / (long double)N;
+    double cr = (double)cosl(ang), ci = (double)sinl(ang);
+    c->twist[2 * j] = cr;
+    c->twist[2 * j + 1] = ci;
+    c->untwist[2 * j] = cr / (double)M;
+    c->untwist[2 * j + 1] = -ci / (double)M;
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* key generation                                                       */
+
+static uint32_t rows_of(const orc_params* p) { return (p->k + 1) * p->pbs_level; }
+
+typedef struct {
+  orc_ctx* c;
+} keygen_arg;
+
+static void bsk_range(void* a, size_t lo, size_t hi) {
+  orc_ctx* c = ((keygen_arg*)a)->c;
+  const orc_params* p = &c->p;
+  const uint32_t N = p->N, k = p->k, rows = rows_of(p), L = p->pbs_level;
+  double* spec = (double*)malloc(sizeof(double) * 2 * c->M);
+  int64_t* tmp = (int64_t*)malloc(sizeof(int64_t) * N);
+  for (size_t i = lo; i < hi; ++i) {
+    for (uint32_t r = 0; r < rows; ++r) {
+      const uint32_t comp = r / L, lev = r % L + 1;
+      uint64_t* row = c->bsk + (((size_t)i * rows + r) * (k + 1)) * N;
+      uint64_t* body = row + (size_t)k * N;
+      memset(body, 0, sizeof(uint64_t) * N);
+      for (uint32_t q = 0; q < k; ++q) {
+        uint64_t* mask = row + (size_t)q * N;
+        for (uint32_t cc = 0; cc < N; ++cc)
+          mask[cc] = orc_rand_u64(c->seed, D_BSK_MASK,
+                                  (((uint64_t)i * rows + r) * k + q) * N + cc);
+        poly_mul_binary_acc(body, mask, c->sk_glwe + (size_t)q * N, N);
+      }
+      for (uint32_t cc = 0; cc < N; ++cc)
+        body[cc] += (uint64_t)orc_tuniform(c->seed, D_BSK_NOISE,
+                                           ((uint64_t)i * rows + r) * N + cc,
+                                           p->glwe_noise_log2);
+      if (c->sk_small[i]) {
+        const uint64_t g = UINT64_C(1) << (64 - p->pbs_base_log * lev);
+        row[(size_t)comp * N] += g; /* constant coefficient of component comp */
+      }
+      for (uint32_t o = 0; o <= k; ++o) {
+        const uint64_t* poly = row + (size_t)o * N;
+        for (uint32_t cc = 0; cc < N; ++cc) tmp[cc] = (int64_t)poly[cc];
+        forward_i64(c, tmp, spec);
+        memcpy(c->bskf + (((size_t)i * rows + r) * (k + 1) + o) * 2 * c->M, spec,
+               sizeof(double) * 2 * c->M);
+      }
+    }
+  }
+  free(spec);
+  free(tmp);
+}
+
+static void ksk_range(void* a, size_t lo, size_t hi) {
+  orc_ctx* c = ((keygen_arg*)a)->c;
+  const orc_params* p = &c->p;
+  const uint32_t n = p->n, L = p->ks_level;
+  for (size_t j = lo; j < hi; ++j) {
+    for (uint32_t l = 0; l < L; ++l) {
+      uint64_t* row = c->ksk + ((size_t)j * L + l) * (n + 1);
+      uint64_t b = 0;
+      for (uint32_t cc = 0; cc < n; ++cc) {
+        row[cc] = orc_rand_u64(c->seed, D_KSK_MASK, ((uint64_t)j * L + l) * n + cc);
+        if (c->sk_small[cc]) b += row[cc];
+      }
+      b += (uint64_t)orc_tuniform(c->seed, D_KSK_NOISE, (uint64_t)j * L + l,
+                                  p->lwe_noise_log2);
+      if (c->sk_glwe[j]) b += UINT64_C(1) << (64 - p->ks_base_log * (l + 1));
+      row[n] = b;
+    }
+  }
+}
+
+orc_ctx* orc_create(const orc_params* p, uint64_t seed, int threads) {
+  orc_ctx* c = (orc_ctx*)calloc(1, sizeof(orc_ctx));
+  c->p = *p;
+  c->seed = seed;
+  const uint32_t n = p->n, N = p->N, k = p->k, rows = rows_of(p);
+  build_tables(c);
+  c->sk_small = (uint8_t*)malloc(n);
+  for (uint32_t i = 0; i < n; ++i) c->sk_small[i] = (uint8_t)(orc_rand_u64(seed, D_SK_SMALL, i) & 1);
+  c->sk_glwe = (uint8_t*)malloc((size_t)k * N);
+  for (uint32_t j = 0; j < k * N; ++j) c->sk_glwe[j] = (uint8_t)(orc_rand_u64(seed, D_SK_GLWE, j) & 1);
+  c->bsk = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n * rows * (k + 1) * N);
+  c->bskf = (double*)malloc(sizeof(double) * (size_t)n * rows * (k + 1) * N);
+  c->ksk = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)k * N * p->ks_level * (n + 1));
+  keygen_arg ka = {c};
+  parallel_for(n, threads, bsk_range, &ka);
+  parallel_for((size_t)k * N, threads, ksk_range, &ka);
+  return c;
+}
+
+void orc_destroy(orc_ctx* c) {
+  if (!c) return;
+  free(c->sk_small);
+  free(c->sk_glwe);
+  free(c->bsk);
+  free(c->bskf);
+  free(c->ksk);
+  free(c->tw);
+  free(c->twist);
+  free(c->untwist);
+  free(c);
+}
+
+const orc_params* orc_get_params(const orc_ctx* c) { return &c->p; }
+const uint8_t* orc_sk_small(const orc_ctx* c) { return c->sk_small; }
+const uint8_t* orc_sk_glwe(const orc_ctx* c) { return c->sk_glwe; }
+const uint64_t* orc_ksk(const orc_ctx* c) { return c->ksk; }
+const uint64_t* orc_bsk(const orc_ctx* c) { return c->bsk; }
+const double* orc_bskf(const orc_ctx* c) { return c->bskf; }
+
+/* ------------------------------------------------------------------ */
+/* encryption                                                           */
+
+static inline uint64_t delta(void) { return UINT64_C(1) << 59; } /* 2^64 / 32 */
+
+void orc_encrypt_at(const orc_ctx* c, int32_t value, uint64_t counter, uint64_t* out) {
+  const uint32_t kN = c->p.k * c->p.N;
+  uint64_t b = 0;
+  for (uint32_t j = 0; j < kN; ++j) {
+    out[j] = orc_rand_u64(c->seed, D_ENC_MASK, counter * kN + j);
+    if (c->sk_glwe[j]) b += out[j];
+  }
+  b += (uint64_t)orc_tuniform(c->seed, D_ENC_NOISE, counter, c->p.glwe_noise_log2);
+  b += (uint64_t)(int64_t)value * delta();
+  out[kN] = b;
+}
+
+void orc_trivial(const orc_ctx* c, int32_t value, uint64_t* out) {
+  const uint32_t kN = c->p.k * c->p.N;
+  memset(out, 0, sizeof(uint64_t) * kN);
+  out[kN] = (uint64_t)(int64_t)value * delta();
+}
+
+uint64_t orc_phase(const orc_ctx* c, const uint64_t* lwe) {
+  const uint32_t kN = c->p.k * c->p.N;
+  uint64_t s = 0;
+  for (uint32_t j = 0; j < kN; ++j)
+    if (c->sk_glwe[j]) s += lwe[j];
+  return lwe[kN] - s;
+}
+
+uint64_t orc_phase_small(const orc_ctx* c, const uint64_t* lwe) {
+  uint64_t s = 0;
+  for (uint32_t j = 0; j < c->p.n; ++j)
+    if (c->sk_small[j]) s += lwe[j];
+  return lwe[c->p.n] - s;
+}
+
+int32_t orc_decrypt(const orc_ctx* c, const uint64_t* lwe) {
+  uint64_t ph = orc_phase(c, lwe);
+  return (int32_t)(((ph + (delta() >> 1)) >> 59) & 31);
+}
+
+/* ------------------------------------------------------------------ */
+/* PBS pieces                                                           */
+
+void orc_keyswitch(const orc_ctx* c, const uint64_t* in, uint64_t* out) {
+  const orc_params* p = &c->p;
+  const uint32_t kN = p->k * p->N, n = p->n, L = p->ks_level;
+  int64_t dig[64];
+  memset(out, 0, sizeof(uint64_t) * n);
+  out[n] = in[kN];
+  for (uint32_t j = 0; j < kN; ++j) {
+    decompose(in[j], p->ks_base_log, L, dig);
+    for (uint32_t l = 0; l < L; ++l) {
+      if (!dig[l]) continue;
+      const uint64_t d = (uint64_t)dig[l];
+      const uint64_t* row = c->ksk + ((size_t)j * L + l) * (n + 1);
+      for (uint32_t cc = 0; cc <= n; ++cc) out[cc] -= d * row[cc];
+    }
+  }
+}
+
+void orc_modswitch(const orc_ctx* c, const uint64_t* in, uint32_t* out) {
+  uint32_t log2N2 = 1;
+  while ((1u << log2N2) < 2 * c->p.N) ++log2N2;
+  const uint32_t shift = 64 - log2N2;
+  for (uint32_t j = 0; j <= c->p.n; ++j)
+    out[j] = (uint32_t)(((in[j] + (UINT64_C(1) << (shift - 1))) >> shift) & ((1u << log2N2) - 1));
+}
+
+void orc_test_poly(const orc_ctx* c, const int32_t lut[16], uint64_t* tp) {
+  const uint32_t N = c->p.N;
+  const uint32_t box = N / 16, half = N / 32;
+  for (uint32_t j = 0; j < N; ++j) {
+    uint32_t t = j + half; /* tp = X^{-half} * aligned boxes */
+    if (t < N)
+      tp[j] = (uint64_t)(int64_t)lut[t / box] * delta();
+    else
+      tp[j] = (uint64_t)0 - (uint64_t)(int64_t)lut[(t - N) / box] * delta();
+  }
+}
+
+static void external_product_fft(const orc_ctx* c, size_t i, const uint64_t* glwe_in,
+                                 uint64_t* glwe_out, double* specs /* rows*2M */,
+                                 double* acc /* 2M */, int64_t* dig /* L*N */) {
+  const orc_params* p = &c->p;
+  const uint32_t N = p->N, k = p->k, L = p->pbs_level, rows = rows_of(p), M = c->M;
+  int64_t dl[64];
+  for (uint32_t comp = 0; comp <= k; ++comp) {
+    const uint64_t* poly = glwe_in + (size_t)comp * N;
+    for (uint32_t j = 0; j < N; ++j) {
+      decompose(poly[j], p->pbs_base_log, L, dl);
+      for (uint32_t l = 0; l < L; ++l) dig[(size_t)l * N + j] = dl[l];
+    }
+    for (uint32_t l = 0; l < L; ++l)
+      forward_i64(c, dig + (size_t)l * N, specs + (size_t)(comp * L + l) * 2 * M);
+  }
+  for (uint32_t o = 0; o <= k; ++o) {
+    memset(acc, 0, sizeof(double) * 2 * M);
+    for (uint32_t r = 0; r < rows; ++r) {
+      const double* d = specs + (size_t)r * 2 * M;
+      const double* b = c->bskf + ((i * rows + r) * (k + 1) + o) * 2 * M;
+      for (uint32_t f = 0; f < M; ++f) {
+        double ar = acc[2 * f], ai = acc[2 * f + 1];
+        const double dr = d[2 * f], di = d[2 * f + 1];
+        const double br = b[2 * f], bi = b[2 * f + 1];
+        ar = fma(dr, br, ar);
+        ar = fma(-di, bi, ar);
+        ai = fma(dr, bi, ai);
+        ai = fma(di, br, ai);
+        acc[2 * f] = ar;
+        acc[2 * f + 1] = ai;
+      }
+    }
+    backward_torus(c, acc, glwe_out + (size_t)o * N);
+  }
+}
+
+static void external_product_exact(const orc_ctx* c, size_t i, const uint64_t* glwe_in,
+                                   uint64_t* glwe_out, int64_t* dig) {
+  const orc_params* p = &c->p;
+  const uint32_t N = p->N, k = p->k, L = p->pbs_level, rows = rows_of(p);
+  int64_t dl[64];
+  memset(glwe_out, 0, sizeof(uint64_t) * (k + 1) * N);
+  for (uint32_t comp = 0; comp <= k; ++comp) {
+    const uint64_t* poly = glwe_in + (size_t)comp * N;
+    for (uint32_t j = 0; j < N; ++j) {
+      decompose(poly[j], p->pbs_base_log, L, dl);
+      for (uint32_t l = 0; l < L; ++l) dig[(size_t)l * N + j] = dl[l];
+    }
+    for (uint32_t l = 0; l < L; ++l) {
+      const uint32_t r = comp * L + l;
+      for (uint32_t o = 0; o <= k; ++o)
+        poly_mul_small_acc(glwe_out + (size_t)o * N, dig + (size_t)l * N,
+                           c->bsk + ((i * rows + r) * (k + 1) + o) * N, N);
+    }
+  }
+}
+
+void orc_blind_rotate(const orc_ctx* c, const uint32_t* ms, const uint64_t* tp,
+                      uint64_t* acc, int mode) {
+  const orc_params* p = &c->p;
+  const uint32_t N = p->N, k = p->k, n = p->n, M = c->M;
+  const size_t glen = (size_t)(k + 1) * N;
+  memset(acc, 0, sizeof(uint64_t) * (size_t)k * N);
+  poly_rotate(tp, acc + (size_t)k * N, N, (2 * N - ms[n]) % (2 * N));
+  uint64_t* diff = (uint64_t*)malloc(sizeof(uint64_t) * glen);
+  uint64_t* ext = (uint64_t*)malloc(sizeof(uint64_t) * glen);
+  double* specs = (double*)malloc(sizeof(double) * 2 * M * rows_of(p));
+  double* facc = (double*)malloc(sizeof(double) * 2 * M);
+  int64_t* dig = (int64_t*)malloc(sizeof(int64_t) * N * p->pbs_level);
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t a = ms[i];
+    if (a == 0) continue;
+    for (uint32_t comp = 0; comp <= k; ++comp) {
+      poly_rotate(acc + (size_t)comp * N, diff + (size_t)comp * N, N, a);
+      for (uint32_t j = 0; j < N; ++j) diff[(size_t)comp * N + j] -= acc[(size_t)comp * N + j];
+    }
+    if (mode == 0)
+      external_product_fft(c, i, diff, ext, specs, facc, dig);
+    else
+      external_product_exact(c, i, diff, ext, dig);
+    for (size_t j = 0; j < glen; ++j) acc[j] += ext[j];
+  }
+  free(diff);
+  free(ext);
+  free(specs);
+  free(facc);
+  free(dig);
+}
+
+void orc_sample_extract(const orc_ctx* c, const uint64_t* glwe, uint64_t* out) {
+  const uint32_t N = c->p.N, k = c->p.k;
+  for (uint32_t q = 0; q < k; ++q) {
+    const uint64_t* a = glwe + (size_t)q * N;
+    out[(size_t)q * N] = a[0];
+    for (uint32_t j = 1; j < N; ++j) out[(size_t)q * N + j] = (uint64_t)0 - a[N - j];
+  }
+  out[(size_t)k * N] = glwe[(size_t)k * N];
+}
+
+void orc_pbs(const orc_ctx* c, const uint64_t* in, const int32_t lut[16], uint64_t* out,
+             int mode) {
+  const orc_params* p = &c->p;
+  uint64_t* small = (uint64_t*)malloc(sizeof(uint64_t) * (p->n + 1));
+  uint32_t* ms = (uint32_t*)malloc(sizeof(uint32_t) * (p->n + 1));
+  uint64_t* tp = (uint64_t*)malloc(sizeof(uint64_t) * p->N);
+  uint64_t* acc = (uint64_t*)malloc(sizeof(uint64_t) * (p->k + 1) * p->N);
+  orc_keyswitch(c, in, small);
+  orc_modswitch(c, small, ms);
+  orc_test_poly(c, lut, tp);
+  orc_blind_rotate(c, ms, tp, acc, mode);
+  orc_sample_extract(c, acc, out);
+  free(small);
+  free(ms);
+  free(tp);
+  free(acc);
+}
+
+typedef struct {
+  const orc_ctx* c;
+  const uint64_t* in;
+  const int32_t* luts;
+  uint64_t* out;
+  int mode;
+} pbs_batch_arg;
+
+static void pbs_range(void* a, size_t lo, size_t hi) {
+  pbs_batch_arg* b = (pbs_batch_arg*)a;
+  const size_t len = (size_t)b->c->p.k * b->c->p.N + 1;
+  for (size_t t = lo; t < hi; ++t)
+    orc_pbs(b->c, b->in + t * len, b->luts + 16 * t, b->out + t * len, b->mode);
+}
+
+void orc_pbs_batch(const orc_ctx* c, size_t count, const uint64_t* in, const int32_t* luts,
+                   uint64_t* out, int mode, int threads) {
+  pbs_batch_arg a = {c, in, luts, out, mode};
+  parallel_for(count, threads, pbs_range, &a);
+}
