@@ -266,7 +266,7 @@ static void fft_dit_inverse(const orc_ctx* c, double* x) {
 
 static inline uint64_t f64_to_torus(double y) {
   const double two64 = 18446744073709551616.0;
-  const double inv64 = 5.42101086242752217e-20; /* 2^-64 */
+  const double inv64 = 0x1p-64;
   double r = rint(y * inv64);
   double d = y - r * two64;
   if (d >= 9223372036854775808.0) d -= two64;

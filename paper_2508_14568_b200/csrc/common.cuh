@@ -1,0 +1,113 @@
+// Shared device/host definitions for the B200 TFHE PBS path.
+//
+// Parameter set: q = 2^64, plaintext space Z_32 with the
+// padding bit (proj/include/leuven/lut.hpp:9-13, kPlaintextModulus = 32),
+// Delta = 2^59; GLWE k = 1, N = 2048; BSK gadget base 2^23, 1 level; KSK
+// gadget base 2^3, 5 levels; small LWE dimension n (runtime, default 880).
+// Everything is q = 2^64 integer arithmetic except the blind-rotation
+// external product, which uses an f64 negacyclic FFT whose operation order
+// is fixed (see fft.cuh) so results are bit-identical to the CPU oracle.
+#pragma once
+
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define LV_HD __host__ __device__ __forceinline__
+#else
+#define LV_HD inline
+#endif
+
+namespace lvb {
+
+constexpr uint32_t kN = 2048;          // GLWE polynomial size
+constexpr uint32_t kM = kN / 2;        // complex FFT size (negacyclic fold)
+constexpr uint32_t kLogM = 10;
+constexpr uint32_t kK = 1;             // GLWE dimension
+constexpr uint32_t kBig = kK * kN;     // big-key LWE mask length
+constexpr uint32_t kBigStride = kBig + 8;  // pool row stride in u64 (16448 B, 64 B aligned)
+constexpr uint32_t kPbsBaseLog = 23;
+constexpr uint32_t kPbsLevel = 1;
+constexpr uint32_t kRows = (kK + 1) * kPbsLevel;  // GGSW rows
+constexpr uint32_t kKsBaseLog = 3;
+constexpr uint32_t kKsLevel = 5;
+constexpr uint32_t kLog2N2 = 12;       // log2(2N)
+constexpr uint64_t kDelta = 1ull << 59;
+
+// Philox domains (shared by specification with the oracle).
+enum Domain : uint32_t {
+  kDomSkSmall = 1,
+  kDomSkGlwe = 2,
+  kDomBskMask = 3,
+  kDomBskNoise = 4,
+  kDomKskMask = 5,
+  kDomKskNoise = 6,
+  kDomEncMask = 7,
+  kDomEncNoise = 8,
+};
+
+// Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11): key = seed,
+// counter = {idx_lo, idx_hi, domain, 0}; returns words 0,1 as a u64.
+LV_HD uint64_t philox_u64(uint64_t seed, uint32_t domain, uint64_t idx) {
+  uint32_t c0 = (uint32_t)idx, c1 = (uint32_t)(idx >> 32), c2 = domain, c3 = 0;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+    const uint32_t n1 = (uint32_t)p1;
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    const uint32_t n3 = (uint32_t)p0;
+    c0 = n0;
+    c1 = n1;
+    c2 = n2;
+    c3 = n3;
+  }
+  return ((uint64_t)c1 << 32) | c0;
+}
+
+// TUniform(b): integers in [-2^b, 2^b] with half weight on the endpoints.
+LV_HD int64_t tuniform(uint64_t seed, uint32_t domain, uint64_t idx, uint32_t b) {
+  const uint64_t x = philox_u64(seed, domain, idx) & ((1ull << (b + 2)) - 1);
+  return (int64_t)(x >> 1) + (int64_t)(x & 1) - ((int64_t)1 << b);
+}
+
+// Closest-representable signed gadget digit, 1 level (digits in [-B/2, B/2)).
+LV_HD int64_t decomp1(uint64_t x, uint32_t base_log) {
+  const uint32_t shift = 64 - base_log;
+  const uint64_t v = (x + (1ull << (shift - 1))) >> shift;
+  const int64_t half = (int64_t)1 << (base_log - 1);
+  int64_t d = (int64_t)v;
+  if (d >= half) d -= (int64_t)1 << base_log;
+  return d;
+}
+
+// Multi-level variant: digits[0] has weight q/B (most significant).
+template <int L>
+LV_HD void decomp(uint64_t x, uint32_t base_log, int64_t* digits) {
+  const uint32_t shift = 64 - base_log * L;
+  uint64_t v = (x + (1ull << (shift - 1))) >> shift;
+  const uint64_t mask = (1ull << base_log) - 1;
+  const int64_t half = (int64_t)1 << (base_log - 1);
+#pragma unroll
+  for (int l = L - 1; l >= 0; --l) {
+    int64_t d = (int64_t)(v & mask);
+    v >>= base_log;
+    if (d >= half) {
+      d -= (int64_t)1 << base_log;
+      v += 1;
+    }
+    digits[l] = d;
+  }
+}
+
+LV_HD uint32_t modswitch(uint64_t a) {
+  constexpr uint32_t shift = 64 - kLog2N2;
+  return (uint32_t)(((a + (1ull << (shift - 1))) >> shift) & ((1u << kLog2N2) - 1));
+}
+
+}  // namespace lvb

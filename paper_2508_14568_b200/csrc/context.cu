@@ -1,0 +1,827 @@
+// Host runtime: context lifecycle and key generation, the device ciphertext
+// pool, the Backend operations (proj/include/leuven/backend.hpp:54-76) and
+// the batched PBS driver, exposed through the C ABI in include/leuven_b200.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "context.hpp"
+
+namespace lvb {
+
+thread_local std::string g_last_error;
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(LV_ERR_CUDA, std::string("CUDA error ") + cudaGetErrorString(e) + " at " + what);
+}
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return LV_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return LV_ERR_CUDA;
+  }
+}
+
+uint32_t ms_stride(const lv_ctx* c) { return (c->p.n + 1 + 7) / 8 * 8; }
+
+// ---------------------------------------------------------------- pool
+static void pool_grow(lv_ctx* c, size_t need) {
+  if (need <= c->pool_cap) return;
+  size_t cap = std::max<size_t>(need, (size_t)c->pool_cap * 2);
+  cap = std::max<size_t>(cap, 1024);
+  uint64_t* np = nullptr;
+  LV_CUDA(cudaMalloc(&np, cap * kBigStride * sizeof(uint64_t)));
+  if (c->d_pool) {
+    LV_CUDA(cudaMemcpyAsync(np, c->d_pool, (size_t)c->pool_cap * kBigStride * sizeof(uint64_t),
+                            cudaMemcpyDeviceToDevice, c->stream));
+    LV_CUDA(cudaStreamSynchronize(c->stream));
+    LV_CUDA(cudaFree(c->d_pool));
+  }
+  c->d_pool = np;
+  for (size_t s = cap; s-- > c->pool_cap;) c->free_slots.push_back((uint32_t)s);
+  c->live.resize(cap, 0);
+  c->ledgers.resize(cap);
+  c->pool_cap = (uint32_t)cap;
+}
+
+std::vector<lv_ct> pool_alloc(lv_ctx* c, size_t count) {
+  if (c->free_slots.size() < count) pool_grow(c, (size_t)c->pool_cap + count - c->free_slots.size());
+  std::vector<lv_ct> out(count);
+  for (size_t i = 0; i < count; ++i) {
+    out[i] = c->free_slots.back();
+    c->free_slots.pop_back();
+    c->live[out[i]] = 1;
+    c->ledgers[out[i]] = NoiseLedger();
+  }
+  return out;
+}
+
+void pool_free(lv_ctx* c, const lv_ct* cts, size_t count) {
+  for (size_t i = 0; i < count; ++i) {
+    if (cts[i] < c->pool_cap && c->live[cts[i]]) {
+      c->live[cts[i]] = 0;
+      c->ledgers[cts[i]] = NoiseLedger();
+      c->free_slots.push_back(cts[i]);
+    }
+  }
+}
+
+void check_handles(const lv_ctx* c, const lv_ct* cts, size_t count) {
+  for (size_t i = 0; i < count; ++i)
+    if (cts[i] >= c->pool_cap || !c->live[cts[i]])
+      throw Error(LV_ERR_INVALID_HANDLE, "invalid ciphertext handle " + std::to_string(cts[i]));
+}
+
+// ---------------------------------------------------------------- LUTs
+// Test polynomial of a Lut16 (lut.hpp:15-24): boxes of N/16 coefficients
+// holding entries[m] * Delta, rotated by half a box (X^{-N/32}) so the
+// rounding window of message m is centred; the negacyclic wrap of X^N = -1
+// yields -entries[x-16] for x in [16,32) exactly as negacyclic_eval does
+// (proj/src/lut.cpp:9-16).
+static void build_test_poly(const std::array<int32_t, 16>& e, uint64_t* tp) {
+  const uint32_t box = kN / 16, half = kN / 32;
+  for (uint32_t j = 0; j < kN; ++j) {
+    const uint32_t t = j + half;
+    tp[j] = t < kN ? (uint64_t)(int64_t)e[t / box] * kDelta
+                   : (uint64_t)0 - (uint64_t)(int64_t)e[(t - kN) / box] * kDelta;
+  }
+}
+
+uint32_t lut_id(lv_ctx* c, const std::array<int32_t, 16>& e) {
+  for (int v : e)
+    if (v < 0 || v >= 32)
+      throw Error(LV_ERR_OUT_OF_RANGE, "lookup entry outside [0,32): " + std::to_string(v));
+  for (size_t i = 0; i < c->luts.size(); ++i)
+    if (c->luts[i] == e) return (uint32_t)i;
+  const uint32_t id = (uint32_t)c->luts.size();
+  if (id >= c->tp_cap) {
+    const uint32_t cap = std::max<uint32_t>(64, c->tp_cap * 2);
+    uint64_t* np = nullptr;
+    LV_CUDA(cudaMalloc(&np, (size_t)cap * kN * sizeof(uint64_t)));
+    if (c->d_tp) {
+      LV_CUDA(cudaMemcpyAsync(np, c->d_tp, (size_t)c->tp_cap * kN * 8, cudaMemcpyDeviceToDevice,
+                              c->stream));
+      LV_CUDA(cudaStreamSynchronize(c->stream));
+      LV_CUDA(cudaFree(c->d_tp));
+    }
+    c->d_tp = np;
+    c->tp_cap = cap;
+  }
+  std::vector<uint64_t> tp(kN);
+  build_test_poly(e, tp.data());
+  LV_CUDA(cudaMemcpyAsync(c->d_tp + (size_t)id * kN, tp.data(), kN * 8, cudaMemcpyHostToDevice,
+                          c->stream));
+  LV_CUDA(cudaStreamSynchronize(c->stream));
+  c->luts.push_back(e);
+  return id;
+}
+
+// ---------------------------------------------------------------- PBS driver
+void launch_pbs_dev(lv_ctx* c, const LinDesc* d_desc, const uint32_t* d_lut, const BrOut* d_out,
+                    uint32_t count, cudaEvent_t ks_done) {
+  if (!count) return;
+  const uint32_t stride = ms_stride(c);
+  uint16_t* d_ms = c->ms.get((size_t)count * stride);
+  KsArgs ka{d_desc, c->d_pool, kBigStride, c->d_ksk, c->p.n, count, d_ms, stride, nullptr};
+  const uint32_t row = c->p.n + 1;
+  for (uint32_t off = 0; off < count; off += 65535u * kKsItems) {
+    const uint32_t cnt = std::min<uint32_t>(count - off, 65535u * kKsItems);
+    KsArgs k2 = ka;
+    k2.desc = d_desc + off;
+    k2.count = cnt;
+    k2.ms = d_ms + (size_t)off * stride;
+    dim3 grid((row + 127) / 128, (cnt + kKsItems - 1) / kKsItems);
+    keyswitch_kernel<<<grid, 128, 0, c->stream>>>(k2);
+  }
+  LV_CUDA(cudaGetLastError());
+  if (ks_done) LV_CUDA(cudaEventRecord(ks_done, c->stream));
+  BrArgs ba{d_ms, stride, d_lut, c->d_tp, c->d_bskf, c->d_tw, c->d_twist, c->p.n,
+            c->d_pool, kBigStride, d_out};
+  blind_rotate_kernel<<<count, 128, blind_rotate_smem_bytes(c->p.n), c->stream>>>(ba);
+  LV_CUDA(cudaGetLastError());
+}
+
+void run_pbs_items(lv_ctx* c, const std::vector<PbsItem>& items) {
+  const size_t count = items.size();
+  if (!count) return;
+  std::vector<LinDesc> d(count);
+  std::vector<uint32_t> l(count);
+  std::vector<BrOut> o(count);
+  for (size_t i = 0; i < count; ++i) {
+    d[i] = items[i].in;
+    l[i] = items[i].lut;
+    o[i] = items[i].out;
+  }
+  LinDesc* dd = c->desc.get(count);
+  uint32_t* dl = c->lut_item.get(count);
+  BrOut* dout = c->br_out.get(count);
+  LV_CUDA(cudaMemcpyAsync(dd, d.data(), count * sizeof(LinDesc), cudaMemcpyHostToDevice, c->stream));
+  LV_CUDA(cudaMemcpyAsync(dl, l.data(), count * 4, cudaMemcpyHostToDevice, c->stream));
+  LV_CUDA(cudaMemcpyAsync(dout, o.data(), count * sizeof(BrOut), cudaMemcpyHostToDevice, c->stream));
+  launch_pbs_dev(c, dd, dl, dout, (uint32_t)count);
+  LV_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+void launch_linear_dev(lv_ctx* c, const LinOut* d_ops, uint32_t count) {
+  if (!count) return;
+  for (uint32_t off = 0; off < count; off += 65535u) {
+    const uint32_t cnt = std::min<uint32_t>(count - off, 65535u);
+    LinArgs la{d_ops + off, c->d_pool, kBigStride, cnt};
+    linear_kernel<<<dim3(2, cnt), 1024, 0, c->stream>>>(la);
+  }
+  LV_CUDA(cudaGetLastError());
+}
+
+void run_linear(lv_ctx* c, const std::vector<LinOut>& ops) {
+  if (ops.empty()) return;
+  LinOut* d = c->lin_ops.get(ops.size());
+  LV_CUDA(cudaMemcpyAsync(d, ops.data(), ops.size() * sizeof(LinOut), cudaMemcpyHostToDevice,
+                          c->stream));
+  launch_linear_dev(c, d, (uint32_t)ops.size());
+  LV_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+static LinDesc single(uint32_t slot, int32_t coef = 1, int32_t body = 0) {
+  LinDesc d{};
+  d.slot[0] = slot;
+  d.coef[0] = coef;
+  d.nterms = 1;
+  d.body_const = body;
+  return d;
+}
+
+static void check_plaintext(int v) {  // backend.cpp:17-21
+  if (v < 0 || v >= 32)
+    throw Error(LV_ERR_OUT_OF_RANGE, "plaintext outside [0,32): " + std::to_string(v));
+}
+
+static void encrypt_into(lv_ctx* c, const int32_t* values, const std::vector<lv_ct>& slots,
+                         bool trivial) {
+  const size_t count = slots.size();
+  if (!count) return;
+  uint32_t* ds = c->u32a.get(count);
+  int32_t* dv = c->i32a.get(count);
+  LV_CUDA(cudaMemcpyAsync(ds, slots.data(), count * 4, cudaMemcpyHostToDevice, c->stream));
+  LV_CUDA(cudaMemcpyAsync(dv, values, count * 4, cudaMemcpyHostToDevice, c->stream));
+  EncArgs ea{c->d_pool, kBigStride, ds, dv, c->d_sk_glwe, c->seed, c->enc_counter,
+             c->p.glwe_noise_log2, trivial ? 1 : 0};
+  encrypt_kernel<<<(uint32_t)count, 256, 0, c->stream>>>(ea);
+  LV_CUDA(cudaGetLastError());
+  LV_CUDA(cudaStreamSynchronize(c->stream));
+  if (!trivial) c->enc_counter += count;
+}
+
+static void upload_rows(lv_ctx* c, const uint64_t* host, const std::vector<lv_ct>& slots) {
+  // contiguous runs of slots become one 2D copy each
+  size_t i = 0;
+  while (i < slots.size()) {
+    size_t j = i + 1;
+    while (j < slots.size() && slots[j] == slots[j - 1] + 1) ++j;
+    LV_CUDA(cudaMemcpy2DAsync(c->d_pool + (size_t)slots[i] * kBigStride, kBigStride * 8,
+                              host + i * (kBig + 1), (kBig + 1) * 8, (kBig + 1) * 8, j - i,
+                              cudaMemcpyHostToDevice, c->stream));
+    i = j;
+  }
+}
+
+static void download_rows(lv_ctx* c, const std::vector<lv_ct>& slots, uint64_t* host) {
+  size_t i = 0;
+  while (i < slots.size()) {
+    size_t j = i + 1;
+    while (j < slots.size() && slots[j] == slots[j - 1] + 1) ++j;
+    LV_CUDA(cudaMemcpy2DAsync(host + i * (kBig + 1), (kBig + 1) * 8,
+                              c->d_pool + (size_t)slots[i] * kBigStride, kBigStride * 8,
+                              (kBig + 1) * 8, j - i, cudaMemcpyDeviceToHost, c->stream));
+    i = j;
+  }
+}
+
+static std::vector<uint64_t> phases(lv_ctx* c, const lv_ct* cts, size_t count) {
+  std::vector<uint64_t> ph(count);
+  if (!count) return ph;
+  uint32_t* ds = c->u32a.get(count);
+  uint64_t* dp = c->u64a.get(count);
+  LV_CUDA(cudaMemcpyAsync(ds, cts, count * 4, cudaMemcpyHostToDevice, c->stream));
+  PhaseArgs pa{c->d_pool, kBigStride, ds, c->d_sk_glwe, dp};
+  phase_kernel<<<(uint32_t)count, 256, 0, c->stream>>>(pa);
+  LV_CUDA(cudaGetLastError());
+  LV_CUDA(cudaMemcpyAsync(ph.data(), dp, count * 8, cudaMemcpyDeviceToHost, c->stream));
+  LV_CUDA(cudaStreamSynchronize(c->stream));
+  return ph;
+}
+
+static int32_t decode(uint64_t ph) { return (int32_t)(((ph + (kDelta >> 1)) >> 59) & 31); }
+
+// Budget check of SimBackend::pbs (backend.cpp:62-67).
+static void check_budget(lv_ctx* c, const lv_ct* in, size_t count) {
+  for (size_t i = 0; i < count; ++i) {
+    const int64_t v = c->ledgers[in[i]].variance();
+    if ((double)v > c->p.max_variance_budget)
+      throw Error(LV_ERR_NOISE_BUDGET, "bootstrap input variance " + std::to_string(v) +
+                                           " exceeds budget " +
+                                           std::to_string(c->p.max_variance_budget));
+  }
+}
+
+static void pbs_batch(lv_ctx* c, const lv_ct* in, const uint32_t* luts, size_t count, lv_ct* out) {
+  check_handles(c, in, count);
+  for (size_t i = 0; i < count; ++i)
+    if (luts[i] >= c->luts.size()) throw Error(LV_ERR_INVALID_PARAMS, "unknown lut id");
+  check_budget(c, in, count);
+  std::vector<lv_ct> dst = pool_alloc(c, count);
+  std::vector<PbsItem> items(count);
+  for (size_t i = 0; i < count; ++i) {
+    items[i].in = single(in[i]);
+    items[i].lut = luts[i];
+    items[i].out = BrOut{0, dst[i], kNoSlot, kNoSlot, kNoSlot, 0};
+  }
+  run_pbs_items(c, items);
+  for (size_t i = 0; i < count; ++i) {
+    c->ledgers[dst[i]] = NoiseLedger::fresh(c->next_source++);
+    out[i] = dst[i];
+  }
+  c->pbs_count += count;
+}
+
+static void build_tables(lv_ctx* c) {
+  const long double PI = 3.141592653589793238462643383279502884L;
+  std::vector<double2> tw(kM / 2), twist(kM);
+  for (uint32_t t = 0; t < kM / 2; ++t) {
+    const long double ang = 2.0L * PI * (long double)t / (long double)kM;
+    tw[t] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
+  }
+  for (uint32_t j = 0; j < kM; ++j) {
+    const long double ang = PI * (long double)j / (long double)kN;
+    twist[j] = make_double2((double)cosl(ang), (double)sinl(ang));
+  }
+  LV_CUDA(cudaMalloc(&c->d_tw, tw.size() * sizeof(double2)));
+  LV_CUDA(cudaMalloc(&c->d_twist, twist.size() * sizeof(double2)));
+  LV_CUDA(cudaMemcpy(c->d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  LV_CUDA(cudaMemcpy(c->d_twist, twist.data(), twist.size() * sizeof(double2), cudaMemcpyHostToDevice));
+}
+
+static void keygen(lv_ctx* c) {
+  const uint32_t n = c->p.n;
+  LV_CUDA(cudaMalloc(&c->d_sk_small, n));
+  LV_CUDA(cudaMalloc(&c->d_sk_glwe, kBig));
+  keygen_secret_kernel<<<(std::max(n, kBig) + 255) / 256, 256, 0, c->stream>>>(c->seed, n, c->d_sk_small,
+                                                                              c->d_sk_glwe);
+  LV_CUDA(cudaGetLastError());
+  LV_CUDA(cudaMalloc(&c->d_ksk, (size_t)kBig * kKsLevel * (n + 1) * sizeof(uint64_t)));
+  keygen_ksk_kernel<<<kBig * kKsLevel, 256, 0, c->stream>>>(c->seed, n, c->p.lwe_noise_log2,
+                                                            c->d_sk_small, c->d_sk_glwe, c->d_ksk);
+  LV_CUDA(cudaGetLastError());
+  uint64_t* d_bsk = nullptr;
+  LV_CUDA(cudaMalloc(&d_bsk, (size_t)n * kRows * (kK + 1) * kN * sizeof(uint64_t)));
+  keygen_bsk_kernel<<<n * kRows, 256, 0, c->stream>>>(c->seed, c->p.glwe_noise_log2, c->d_sk_small,
+                                                      c->d_sk_glwe, d_bsk);
+  LV_CUDA(cudaGetLastError());
+  LV_CUDA(cudaMalloc(&c->d_bskf, (size_t)n * 32 * 128 * sizeof(double2)));
+  bsk_fourier_kernel<<<n * kRows, 128, 0, c->stream>>>(d_bsk, c->d_tw, c->d_twist, c->d_bskf);
+  LV_CUDA(cudaGetLastError());
+  LV_CUDA(cudaStreamSynchronize(c->stream));
+  LV_CUDA(cudaFree(d_bsk));
+}
+
+std::array<int32_t, 16> eq_lut_entries(int scale) {  // equality.cpp:31-36
+  std::array<int32_t, 16> e{};
+  e[0] = scale;
+  return e;
+}
+
+// build_min_lut (kernel.cpp:28-72): key -> 1 + min(-eq, dv, dh) over the 18
+// packed keys; entries 0..15 are the table, keys 16/17 must be the forced
+// negacyclic images (checked: PackingViolation).
+std::array<int32_t, 16> min_lut_entries(bool negated) {
+  std::array<int32_t, 18> values{};
+  for (int key = 0; key < 18; ++key) {
+    const int eq = key >= 9 ? 1 : 0;
+    const int r = key % 9;
+    const int dv_part = r % 3, dh = r / 3 - 1;
+    const int dv = negated ? 1 - dv_part : dv_part - 1;
+    values[key] = 1 + std::min({-eq, dv, dh});
+  }
+  std::array<int32_t, 16> e{};
+  for (int i = 0; i < 16; ++i) e[i] = ((values[i] % 32) + 32) % 32;
+  for (int k = 16; k < 18; ++k) {
+    const int img = (32 - e[k - 16]) % 32;
+    if (img != ((values[k] % 32) + 32) % 32) throw Error(LV_ERR_PACKING, "min table packing violated");
+  }
+  return e;
+}
+
+}  // namespace lvb
+
+using namespace lvb;
+
+// ====================================================================== C ABI
+extern "C" {
+
+void lv_default_params(lv_params* p) {
+  p->n = 880;
+  p->N = kN;
+  p->k = kK;
+  p->pbs_base_log = kPbsBaseLog;
+  p->pbs_level = kPbsLevel;
+  p->ks_base_log = kKsBaseLog;
+  p->ks_level = kKsLevel;
+  p->lwe_noise_log2 = 44;
+  p->glwe_noise_log2 = 17;
+  p->max_variance_budget = 4000.0;
+}
+
+const char* lv_last_error(void) { return g_last_error.c_str(); }
+int lv_abi_version(void) { return LV_ABI_VERSION; }
+
+int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
+  return guard([&] {
+    lv_params p;
+    if (params)
+      p = *params;
+    else
+      lv_default_params(&p);
+    if (p.N != kN || p.k != kK || p.pbs_base_log != kPbsBaseLog || p.pbs_level != kPbsLevel ||
+        p.ks_base_log != kKsBaseLog || p.ks_level != kKsLevel)
+      throw Error(LV_ERR_INVALID_PARAMS, "parameter set does not match the compiled kernels");
+    if (p.n < 1 || p.n > 4096) throw Error(LV_ERR_INVALID_PARAMS, "n out of range");
+    if (p.max_variance_budget < 1.0)  // backend.hpp:85-88
+      throw Error(LV_ERR_INVALID_PARAMS, "noise budget must be at least 1");
+    int ndev = 0;
+    LV_CUDA(cudaGetDeviceCount(&ndev));
+    if (ndev < 1) throw Error(LV_ERR_CUDA, "no CUDA device");
+    lv_ctx* c = new lv_ctx();
+    try {
+      c->p = p;
+      c->seed = seed;
+      LV_CUDA(cudaGetDevice(&c->device));
+      LV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      LV_CUDA(cudaFuncSetAttribute(blind_rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)blind_rotate_smem_bytes(p.n)));
+      build_tables(c);
+      keygen(c);
+      c->min_lut[0] = lut_id(c, min_lut_entries(false));
+      c->min_lut[1] = lut_id(c, min_lut_entries(true));
+      std::array<int32_t, 16> id{};
+      for (int i = 0; i < 16; ++i) id[i] = i;
+      c->identity_lut = lut_id(c, id);
+      pool_grow(c, 1024);
+    } catch (...) {
+      lv_ctx_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void lv_ctx_destroy(lv_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : {(void*)c->d_sk_small, (void*)c->d_sk_glwe, (void*)c->d_ksk, (void*)c->d_bskf,
+                  (void*)c->d_tw, (void*)c->d_twist, (void*)c->d_tp, (void*)c->d_pool})
+    if (p) cudaFree(p);
+  c->ms.release();
+  c->desc.release();
+  c->lut_item.release();
+  c->br_out.release();
+  c->lin_ops.release();
+  c->u32a.release();
+  c->u32b.release();
+  c->i32a.release();
+  c->u64a.release();
+  c->u64b.release();
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int lv_get_params(lv_ctx* c, lv_params* out) {
+  return guard([&] { *out = c->p; });
+}
+
+int lv_encrypt(lv_ctx* c, const int32_t* values, size_t count, lv_ct* out) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    for (size_t i = 0; i < count; ++i) check_plaintext(values[i]);
+    std::vector<lv_ct> s = pool_alloc(c, count);
+    encrypt_into(c, values, s, false);
+    for (size_t i = 0; i < count; ++i) {
+      c->ledgers[s[i]] = NoiseLedger::fresh(c->next_source++);
+      out[i] = s[i];
+    }
+  });
+}
+
+int lv_trivial(lv_ctx* c, const int32_t* values, size_t count, lv_ct* out) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    for (size_t i = 0; i < count; ++i) check_plaintext(values[i]);
+    std::vector<lv_ct> s = pool_alloc(c, count);
+    encrypt_into(c, values, s, true);
+    for (size_t i = 0; i < count; ++i) out[i] = s[i];
+  });
+}
+
+int lv_decrypt(lv_ctx* c, const lv_ct* cts, size_t count, int32_t* out) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    check_handles(c, cts, count);
+    std::vector<uint64_t> ph = phases(c, cts, count);
+    for (size_t i = 0; i < count; ++i) out[i] = decode(ph[i]);
+  });
+}
+
+int lv_phase(lv_ctx* c, const lv_ct* cts, size_t count, uint64_t* out) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    check_handles(c, cts, count);
+    std::vector<uint64_t> ph = phases(c, cts, count);
+    std::memcpy(out, ph.data(), count * 8);
+  });
+}
+
+static int linear2(lv_ctx* c, const lv_ct* a, const lv_ct* b, size_t count, lv_ct* out, int sign) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    check_handles(c, a, count);
+    check_handles(c, b, count);
+    std::vector<lv_ct> dst = pool_alloc(c, count);
+    std::vector<LinOut> ops(count);
+    for (size_t i = 0; i < count; ++i) {
+      LinOut o{};
+      o.nout = 1;
+      o.out_slot[0] = dst[i];
+      o.d[0].slot[0] = a[i];
+      o.d[0].coef[0] = 1;
+      o.d[0].slot[1] = b[i];
+      o.d[0].coef[1] = sign;
+      o.d[0].nterms = 2;
+      ops[i] = o;
+    }
+    run_linear(c, ops);
+    for (size_t i = 0; i < count; ++i) {
+      NoiseLedger l = c->ledgers[a[i]];
+      l.add_scaled(c->ledgers[b[i]], sign);
+      c->ledgers[dst[i]] = std::move(l);
+      out[i] = dst[i];
+    }
+    c->linear_count += count;
+  });
+}
+
+int lv_add(lv_ctx* c, const lv_ct* a, const lv_ct* b, size_t count, lv_ct* out) {
+  return linear2(c, a, b, count, out, 1);
+}
+int lv_sub(lv_ctx* c, const lv_ct* a, const lv_ct* b, size_t count, lv_ct* out) {
+  return linear2(c, a, b, count, out, -1);
+}
+
+static int scalar_op(lv_ctx* c, const lv_ct* a, const int32_t* k, size_t count, lv_ct* out, bool mul) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    check_handles(c, a, count);
+    std::vector<lv_ct> dst = pool_alloc(c, count);
+    std::vector<LinOut> ops(count);
+    for (size_t i = 0; i < count; ++i) {
+      LinOut o{};
+      o.nout = 1;
+      o.out_slot[0] = dst[i];
+      o.d[0] = single(a[i], mul ? k[i] : 1, mul ? 0 : k[i]);
+      ops[i] = o;
+    }
+    run_linear(c, ops);
+    for (size_t i = 0; i < count; ++i) {
+      NoiseLedger l = c->ledgers[a[i]];
+      if (mul) l.scale(k[i]);
+      c->ledgers[dst[i]] = std::move(l);
+      out[i] = dst[i];
+    }
+    c->linear_count += count;
+  });
+}
+
+int lv_scalar_mul(lv_ctx* c, const lv_ct* a, const int32_t* k, size_t count, lv_ct* out) {
+  return scalar_op(c, a, k, count, out, true);
+}
+int lv_scalar_add(lv_ctx* c, const lv_ct* a, const int32_t* k, size_t count, lv_ct* out) {
+  return scalar_op(c, a, k, count, out, false);
+}
+
+int lv_lut_upload(lv_ctx* c, const int32_t entries[16], uint32_t* id) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    std::array<int32_t, 16> e{};
+    std::memcpy(e.data(), entries, sizeof(e));
+    *id = lut_id(c, e);
+  });
+}
+
+int lv_pbs_batch(lv_ctx* c, const lv_ct* in, const uint32_t* luts, size_t count, lv_ct* out) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    pbs_batch(c, in, luts, count, out);
+  });
+}
+
+int lv_refresh_batch(lv_ctx* c, const lv_ct* in, size_t count, lv_ct* out) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    check_handles(c, in, count);
+    std::vector<uint64_t> ph = phases(c, in, count);
+    for (size_t i = 0; i < count; ++i) {  // backend.cpp:72-80
+      const int32_t v = decode(ph[i]);
+      if (v >= 16)
+        throw Error(LV_ERR_VALUE_OUTSIDE_LUT_HALF,
+                    "refresh needs a value in [0,16), got " + std::to_string(v));
+    }
+    std::vector<uint32_t> luts(count, c->identity_lut);
+    pbs_batch(c, in, luts.data(), count, out);
+    c->refresh_count += count;
+  });
+}
+
+int lv_predict_variance(lv_ctx* c, const lv_ct* cts, const int32_t* coeffs, size_t count,
+                        int64_t* out) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    check_handles(c, cts, count);
+    NoiseLedger comb;
+    for (size_t i = 0; i < count; ++i) comb.add_scaled(c->ledgers[cts[i]], coeffs[i]);
+    *out = comb.variance();
+  });
+}
+
+int lv_ledger_variance(lv_ctx* c, const lv_ct* cts, size_t count, int64_t* out) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    check_handles(c, cts, count);
+    for (size_t i = 0; i < count; ++i) out[i] = c->ledgers[cts[i]].variance();
+  });
+}
+
+int lv_get_stats(lv_ctx* c, lv_stats* out) {
+  return guard([&] {
+    out->pbs_count = c->pbs_count.load();
+    out->refresh_count = c->refresh_count.load();
+    out->linear_op_count = c->linear_count.load();
+  });
+}
+
+int lv_release(lv_ctx* c, const lv_ct* cts, size_t count) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    pool_free(c, cts, count);
+  });
+}
+
+int lv_export(lv_ctx* c, const lv_ct* cts, size_t count, uint64_t* host) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    check_handles(c, cts, count);
+    download_rows(c, std::vector<lv_ct>(cts, cts + count), host);
+    LV_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int lv_import(lv_ctx* c, const uint64_t* host, size_t count, lv_ct* out) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    std::vector<lv_ct> s = pool_alloc(c, count);
+    upload_rows(c, host, s);
+    LV_CUDA(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < count; ++i) {
+      c->ledgers[s[i]] = NoiseLedger::fresh(c->next_source++);
+      out[i] = s[i];
+    }
+  });
+}
+
+int lv_pbs_batch_host(lv_ctx* c, const uint64_t* in, const uint32_t* luts, size_t count,
+                      uint64_t* out) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    for (size_t i = 0; i < count; ++i)
+      if (luts[i] >= c->luts.size()) throw Error(LV_ERR_INVALID_PARAMS, "unknown lut id");
+    std::vector<lv_ct> s = pool_alloc(c, count);
+    upload_rows(c, in, s);
+    std::vector<PbsItem> items(count);
+    for (size_t i = 0; i < count; ++i) {
+      items[i].in = single(s[i]);
+      items[i].lut = luts[i];
+      items[i].out = BrOut{0, s[i], kNoSlot, kNoSlot, kNoSlot, 0};  // in place: KS reads first
+    }
+    std::vector<LinDesc> d(count);
+    std::vector<uint32_t> l(count);
+    std::vector<BrOut> o(count);
+    for (size_t i = 0; i < count; ++i) {
+      d[i] = items[i].in;
+      l[i] = items[i].lut;
+      o[i] = items[i].out;
+    }
+    LinDesc* dd = c->desc.get(count);
+    uint32_t* dl = c->lut_item.get(count);
+    BrOut* dout = c->br_out.get(count);
+    LV_CUDA(cudaMemcpyAsync(dd, d.data(), count * sizeof(LinDesc), cudaMemcpyHostToDevice, c->stream));
+    LV_CUDA(cudaMemcpyAsync(dl, l.data(), count * 4, cudaMemcpyHostToDevice, c->stream));
+    LV_CUDA(cudaMemcpyAsync(dout, o.data(), count * sizeof(BrOut), cudaMemcpyHostToDevice, c->stream));
+    launch_pbs_dev(c, dd, dl, dout, (uint32_t)count);
+    download_rows(c, s, out);
+    LV_CUDA(cudaStreamSynchronize(c->stream));
+    pool_free(c, s.data(), count);
+    c->pbs_count += count;
+  });
+}
+
+// ------------------------------------------------------------- debug / parity
+int lv_debug_keys(lv_ctx* c, uint8_t* sk_small, uint8_t* sk_glwe, uint64_t* ksk, double* bskf_nat) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    const uint32_t n = c->p.n;
+    if (sk_small) LV_CUDA(cudaMemcpy(sk_small, c->d_sk_small, n, cudaMemcpyDeviceToHost));
+    if (sk_glwe) LV_CUDA(cudaMemcpy(sk_glwe, c->d_sk_glwe, kBig, cudaMemcpyDeviceToHost));
+    if (ksk)
+      LV_CUDA(cudaMemcpy(ksk, c->d_ksk, (size_t)kBig * kKsLevel * (n + 1) * 8, cudaMemcpyDeviceToHost));
+    if (bskf_nat) {
+      std::vector<double2> raw((size_t)n * 32 * 128);
+      LV_CUDA(cudaMemcpy(raw.data(), c->d_bskf, raw.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+      // device [i][q*4 + r*2 + o][t] -> oracle [(i*rows + r)*(k+1) + o][f = 8t+q] (re, im)
+      for (size_t i = 0; i < n; ++i)
+        for (uint32_t q = 0; q < 8; ++q)
+          for (uint32_t r = 0; r < 2; ++r)
+            for (uint32_t o = 0; o < 2; ++o)
+              for (uint32_t t = 0; t < 128; ++t) {
+                const double2 v = raw[i * 4096 + (q * 4 + r * 2 + o) * 128 + t];
+                const size_t base = ((i * kRows + r) * (kK + 1) + o) * 2 * kM + 2 * (8 * t + q);
+                bskf_nat[base] = v.x;
+                bskf_nat[base + 1] = v.y;
+              }
+    }
+  });
+}
+
+int lv_debug_keyswitch(lv_ctx* c, const uint64_t* in, size_t count, uint64_t* out_small) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    std::vector<lv_ct> s = pool_alloc(c, count);
+    upload_rows(c, in, s);
+    std::vector<LinDesc> d(count);
+    for (size_t i = 0; i < count; ++i) d[i] = single(s[i]);
+    LinDesc* dd = c->desc.get(count);
+    LV_CUDA(cudaMemcpyAsync(dd, d.data(), count * sizeof(LinDesc), cudaMemcpyHostToDevice, c->stream));
+    const uint32_t row = c->p.n + 1, stride = ms_stride(c);
+    uint64_t* dsmall = c->u64b.get(count * row);
+    uint16_t* dms = c->ms.get(count * stride);
+    KsArgs ka{dd, c->d_pool, kBigStride, c->d_ksk, c->p.n, (uint32_t)count, dms, stride, dsmall};
+    dim3 grid((row + 127) / 128, (uint32_t)((count + kKsItems - 1) / kKsItems));
+    keyswitch_kernel<<<grid, 128, 0, c->stream>>>(ka);
+    LV_CUDA(cudaGetLastError());
+    LV_CUDA(cudaMemcpyAsync(out_small, dsmall, count * row * 8, cudaMemcpyDeviceToHost, c->stream));
+    LV_CUDA(cudaStreamSynchronize(c->stream));
+    pool_free(c, s.data(), count);
+  });
+}
+
+int lv_debug_blind_rotate(lv_ctx* c, const uint32_t* ms, const uint32_t* luts, size_t count,
+                          uint64_t* out) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    const uint32_t row = c->p.n + 1, stride = ms_stride(c);
+    std::vector<uint16_t> h((size_t)count * stride, 0);
+    for (size_t i = 0; i < count; ++i)
+      for (uint32_t j = 0; j < row; ++j) h[i * stride + j] = (uint16_t)ms[i * row + j];
+    std::vector<lv_ct> s = pool_alloc(c, count);
+    std::vector<BrOut> o(count);
+    for (size_t i = 0; i < count; ++i) o[i] = BrOut{0, s[i], kNoSlot, kNoSlot, kNoSlot, 0};
+    uint16_t* dms = c->ms.get(count * stride);
+    uint32_t* dl = c->lut_item.get(count);
+    BrOut* dout = c->br_out.get(count);
+    LV_CUDA(cudaMemcpyAsync(dms, h.data(), h.size() * 2, cudaMemcpyHostToDevice, c->stream));
+    LV_CUDA(cudaMemcpyAsync(dl, luts, count * 4, cudaMemcpyHostToDevice, c->stream));
+    LV_CUDA(cudaMemcpyAsync(dout, o.data(), count * sizeof(BrOut), cudaMemcpyHostToDevice, c->stream));
+    BrArgs ba{dms, stride, dl, c->d_tp, c->d_bskf, c->d_tw, c->d_twist, c->p.n,
+              c->d_pool, kBigStride, dout};
+    blind_rotate_kernel<<<(uint32_t)count, 128, blind_rotate_smem_bytes(c->p.n), c->stream>>>(ba);
+    LV_CUDA(cudaGetLastError());
+    download_rows(c, s, out);
+    LV_CUDA(cudaStreamSynchronize(c->stream));
+    pool_free(c, s.data(), count);
+  });
+}
+
+int lv_debug_fft(lv_ctx* c, const int64_t* poly, double* spec, uint64_t* roundtrip) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    int64_t* dpoly = nullptr;
+    double2* dspec = nullptr;
+    uint64_t* drt = nullptr;
+    LV_CUDA(cudaMalloc(&dpoly, kN * 8));
+    LV_CUDA(cudaMalloc(&dspec, kM * 16));
+    LV_CUDA(cudaMalloc(&drt, kN * 8));
+    LV_CUDA(cudaMemcpy(dpoly, poly, kN * 8, cudaMemcpyHostToDevice));
+    fft_forward_debug_kernel<<<1, 128, 0, c->stream>>>(dpoly, c->d_tw, c->d_twist, dspec);
+    fft_backward_debug_kernel<<<1, 128, 0, c->stream>>>(dspec, c->d_tw, c->d_twist, drt);
+    LV_CUDA(cudaGetLastError());
+    LV_CUDA(cudaStreamSynchronize(c->stream));
+    LV_CUDA(cudaMemcpy(spec, dspec, kM * 16, cudaMemcpyDeviceToHost));
+    LV_CUDA(cudaMemcpy(roundtrip, drt, kN * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dpoly);
+    cudaFree(dspec);
+    cudaFree(drt);
+  });
+}
+
+int lv_bench_pbs(lv_ctx* c, const lv_ct* in, const uint32_t* luts, size_t count, int iters,
+                 float* br_ms, float* ks_ms, float* step_ms) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    check_handles(c, in, count);
+    std::vector<lv_ct> dst = pool_alloc(c, count);
+    std::vector<LinDesc> d(count);
+    std::vector<BrOut> o(count);
+    for (size_t i = 0; i < count; ++i) {
+      d[i] = single(in[i]);
+      o[i] = BrOut{0, dst[i], kNoSlot, kNoSlot, kNoSlot, 0};
+    }
+    LinDesc* dd = c->desc.get(count);
+    uint32_t* dl = c->lut_item.get(count);
+    BrOut* dout = c->br_out.get(count);
+    LV_CUDA(cudaMemcpyAsync(dd, d.data(), count * sizeof(LinDesc), cudaMemcpyHostToDevice, c->stream));
+    LV_CUDA(cudaMemcpyAsync(dl, luts, count * 4, cudaMemcpyHostToDevice, c->stream));
+    LV_CUDA(cudaMemcpyAsync(dout, o.data(), count * sizeof(BrOut), cudaMemcpyHostToDevice, c->stream));
+    cudaEvent_t e0, e1, e2;
+    LV_CUDA(cudaEventCreate(&e0));
+    LV_CUDA(cudaEventCreate(&e1));
+    LV_CUDA(cudaEventCreate(&e2));
+    for (int it = 0; it < iters; ++it) {
+      LV_CUDA(cudaEventRecord(e0, c->stream));
+      launch_pbs_dev(c, dd, dl, dout, (uint32_t)count, e1);
+      LV_CUDA(cudaEventRecord(e2, c->stream));
+      LV_CUDA(cudaEventSynchronize(e2));
+      float a = 0, b = 0, s = 0;
+      LV_CUDA(cudaEventElapsedTime(&a, e0, e1));
+      LV_CUDA(cudaEventElapsedTime(&b, e1, e2));
+      LV_CUDA(cudaEventElapsedTime(&s, e0, e2));
+      if (ks_ms) ks_ms[it] = a;
+      if (br_ms) br_ms[it] = b;
+      if (step_ms) step_ms[it] = s;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    pool_free(c, dst.data(), count);
+    c->pbs_count += (uint64_t)count * iters;
+  });
+}
+
+}  // extern "C"

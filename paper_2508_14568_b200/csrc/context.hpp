@@ -1,0 +1,128 @@
+// lv_ctx: one keyset resident on one GPU, its ciphertext pool, LUT table,
+// host ledgers and counters. Internal to the library (the C ABI in
+// include/leuven_b200.h is the public surface).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/leuven_b200.h"
+#include "kernels.cuh"
+#include "ledger.hpp"
+
+namespace lvb {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define LV_CUDA(x) ::lvb::cuda_check((x), #x)
+
+template <typename T>
+struct DevBuf {  // grow-only device scratch buffer
+  T* p = nullptr;
+  size_t cap = 0;
+  T* get(size_t n) {
+    if (n > cap) {
+      if (p) cudaFree(p);
+      size_t c = std::max<size_t>(n, cap * 2);
+      LV_CUDA(cudaMalloc(&p, c * sizeof(T)));
+      cap = c;
+    }
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// Epilogue of one blind-rotation item (see BrOut in kernels.cuh).
+struct PbsItem {
+  LinDesc in;        // key-switch prologue
+  uint32_t lut;
+  BrOut out;
+};
+
+}  // namespace lvb
+
+struct lv_eqtable {
+  uint64_t length = 0;
+  std::map<char, std::vector<lv_ct>> rows;  // preprocess.hpp:18-39
+};
+
+struct lv_ctx {
+  lv_params p{};
+  uint64_t seed = 0;
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  std::recursive_mutex mu;
+
+  // keys
+  uint8_t* d_sk_small = nullptr;
+  uint8_t* d_sk_glwe = nullptr;
+  uint64_t* d_ksk = nullptr;
+  double2* d_bskf = nullptr;
+  double2* d_tw = nullptr;
+  double2* d_twist = nullptr;
+
+  // LUTs
+  std::vector<std::array<int32_t, 16>> luts;
+  uint64_t* d_tp = nullptr;
+  uint32_t tp_cap = 0;
+
+  // ciphertext pool
+  uint64_t* d_pool = nullptr;
+  uint32_t pool_cap = 0;
+  std::vector<uint32_t> free_slots;
+  std::vector<uint8_t> live;
+  std::vector<lvb::NoiseLedger> ledgers;
+  lvb::NoiseLedger::SourceId next_source = 1;
+  uint64_t enc_counter = 0;
+
+  std::atomic<uint64_t> pbs_count{0}, refresh_count{0}, linear_count{0};
+
+  // scratch
+  lvb::DevBuf<uint16_t> ms;
+  lvb::DevBuf<lvb::LinDesc> desc;
+  lvb::DevBuf<uint32_t> lut_item;
+  lvb::DevBuf<lvb::BrOut> br_out;
+  lvb::DevBuf<lvb::LinOut> lin_ops;
+  lvb::DevBuf<uint32_t> u32a, u32b;
+  lvb::DevBuf<int32_t> i32a;
+  lvb::DevBuf<uint64_t> u64a, u64b;
+
+  std::map<std::string, lvb::PairPlan> plan_cache;
+  uint32_t min_lut[2] = {0, 0};
+  uint32_t identity_lut = 0;
+};
+
+namespace lvb {
+
+uint32_t ms_stride(const lv_ctx* c);
+std::vector<lv_ct> pool_alloc(lv_ctx* c, size_t count);
+void pool_free(lv_ctx* c, const lv_ct* cts, size_t count);
+void check_handles(const lv_ctx* c, const lv_ct* cts, size_t count);
+uint32_t lut_id(lv_ctx* c, const std::array<int32_t, 16>& e);
+
+// Runs count PBS items (key switch with prologue, blind rotation with
+// epilogue) on the context stream. Device pointers of the item arrays are
+// uploaded here; pool slots must already exist.
+void run_pbs_items(lv_ctx* c, const std::vector<PbsItem>& items);
+void launch_pbs_dev(lv_ctx* c, const LinDesc* d_desc, const uint32_t* d_lut, const BrOut* d_out,
+                    uint32_t count, cudaEvent_t ks_done = nullptr);
+void run_linear(lv_ctx* c, const std::vector<LinOut>& ops);
+void launch_linear_dev(lv_ctx* c, const LinOut* d_ops, uint32_t count);
+
+}  // namespace lvb

@@ -1,0 +1,448 @@
+// sm_100a kernels of the TFHE PBS path: blind rotation (f64 FFT external
+// product, GLWE accumulator in shared memory), key switch fused with the
+// modulus switch and with the linear "key formation" prologue, the linear
+// combination kernel behind add/sub/scalar ops and the cell epilogue,
+// encryption / phase, and key generation.
+//
+// Replaces SimBackend::pbs (proj/src/backend.cpp:61-70), whose whole effect
+// is negacyclic_eval(lut, x) (proj/src/lut.cpp:9-16) on a plaintext; here
+// the same table is applied homomorphically to real LWE ciphertexts.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+#include "fft.cuh"
+#include "kernels.cuh"
+
+namespace lvb {
+
+// ------------------------------------------------------------------ BR
+// One CTA (128 threads) blind-rotates one item: ACC = X^{-b~} (0, TP), then
+// for every small-key coefficient i: ACC += BSK_i [x] (X^{a~_i} ACC - ACC),
+// then sample-extracts coefficient 0 into a big-key LWE.
+//
+// Shared memory: acc[2][N] u64 (32 KB) + FFT exchange buffer 2 x kM double2
+// (32 KB) + ms[n+1] u16.
+__global__ void __launch_bounds__(128, 3)
+blind_rotate_kernel(BrArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* acc = reinterpret_cast<uint64_t*>(smem);                   // [2][kN]
+  double2* buf = reinterpret_cast<double2*>(smem + 2 * kN * 8);        // [2][kM]
+  uint16_t* ms = reinterpret_cast<uint16_t*>(smem + 2 * kN * 8 + 2 * kM * 16);
+  const uint32_t t = threadIdx.x;
+  const uint32_t item = blockIdx.x;
+  const uint32_t n = a.n;
+
+  const uint16_t* ms_g = a.ms + (size_t)item * a.ms_stride;
+  for (uint32_t i = t; i <= n; i += 128) ms[i] = ms_g[i];
+  __syncthreads();
+
+  // ACC = X^{-b~} * (0, TP)
+  {
+    const uint64_t* tp = a.test_polys + (size_t)a.lut_of_item[item] * kN;
+    const uint32_t e = (2 * kN - ms[n]) % (2 * kN);
+    for (uint32_t j = t; j < kN; j += 128) {
+      acc[j] = 0;
+      const uint32_t s = (j + 2 * kN - e) % (2 * kN);
+      acc[kN + j] = s < kN ? tp[s] : (uint64_t)0 - tp[s - kN];
+    }
+  }
+
+  const double2* __restrict__ tw = a.twiddles;
+  const double2* __restrict__ twist = a.twist;
+
+  for (uint32_t i = 0; i < n; ++i) {
+    __syncthreads();
+    const uint32_t rot = ms[i];
+    if (rot == 0) continue;  // X^0 - 1 = 0: the external product is exactly 0
+
+    // rotated difference, decomposition, twist (layout fwd A: x = t + 128 r)
+    double2 X[2][8];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const uint64_t* P = acc + p * kN;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const uint32_t x = t + 128 * r;
+        int64_t d[2];
+#pragma unroll
+        for (int hpart = 0; hpart < 2; ++hpart) {
+          const uint32_t j = x + hpart * kM;
+          const uint32_t s = (j + 2 * kN - rot) & (2 * kN - 1);
+          const uint64_t rv = s < kN ? P[s] : (uint64_t)0 - P[s - kN];
+          d[hpart] = decomp1(rv - P[j], kPbsBaseLog);
+        }
+        X[p][r] = cmul(make_double2((double)d[0], (double)d[1]), __ldg(twist + x));
+      }
+    }
+
+    fft_forward<2>(X, buf, tw, t);
+
+    // pointwise MAC against BSK_i (bins 8t + q), layout [i][q*4 + row*2 + o][t]
+    {
+      const double2* bsk = a.bskf + (size_t)i * (32 * 128) + t;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double2 b00 = __ldg(bsk + (q * 4 + 0) * 128);
+        const double2 b01 = __ldg(bsk + (q * 4 + 1) * 128);
+        const double2 b10 = __ldg(bsk + (q * 4 + 2) * 128);
+        const double2 b11 = __ldg(bsk + (q * 4 + 3) * 128);
+        const double2 d0 = X[0][q], d1 = X[1][q];
+        double2 o0, o1;
+        o0.x = __fma_rn(d0.x, b00.x, 0.0);
+        o0.x = __fma_rn(-d0.y, b00.y, o0.x);
+        o0.y = __fma_rn(d0.x, b00.y, 0.0);
+        o0.y = __fma_rn(d0.y, b00.x, o0.y);
+        o0.x = __fma_rn(d1.x, b10.x, o0.x);
+        o0.x = __fma_rn(-d1.y, b10.y, o0.x);
+        o0.y = __fma_rn(d1.x, b10.y, o0.y);
+        o0.y = __fma_rn(d1.y, b10.x, o0.y);
+        o1.x = __fma_rn(d0.x, b01.x, 0.0);
+        o1.x = __fma_rn(-d0.y, b01.y, o1.x);
+        o1.y = __fma_rn(d0.x, b01.y, 0.0);
+        o1.y = __fma_rn(d0.y, b01.x, o1.y);
+        o1.x = __fma_rn(d1.x, b11.x, o1.x);
+        o1.x = __fma_rn(-d1.y, b11.y, o1.x);
+        o1.y = __fma_rn(d1.x, b11.y, o1.y);
+        o1.y = __fma_rn(d1.y, b11.x, o1.y);
+        X[0][q] = o0;
+        X[1][q] = o1;
+      }
+    }
+    __syncthreads();  // forward's last buffer reads precede the inverse's writes
+    fft_inverse<2>(X, buf, tw, t);
+
+    // untwist, back to the torus, accumulate
+    {
+      const uint32_t h = (t >> 4) & 1, u = 16 * (t >> 5) + (t & 15);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int hi = 0; hi < 2; ++hi) {
+          const uint32_t x = u + 64 * (4 * h + q) + 512 * hi;
+          const double2 tv = __ldg(twist + x);
+          const double2 ut = make_double2(__dmul_rn(tv.x, 0x1p-10), __dmul_rn(-tv.y, 0x1p-10));
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            const double2 z = cmul(X[p][4 * hi + q], ut);
+            acc[p * kN + x] += f64_to_torus(z.x);
+            acc[p * kN + x + kM] += f64_to_torus(z.y);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // sample extract coefficient 0 (a'_0 = A_0, a'_j = -A_{N-j}, b' = B_0) + epilogue
+  const BrOut o = a.outs[item];
+  const uint32_t S = a.pool_stride;
+  if (o.mode == 0) {
+    uint64_t* out = a.pool + (size_t)o.slot_a * S;
+    for (uint32_t j = t; j <= kN; j += 128) {
+      uint64_t v = j == 0 ? acc[0] : (j == kN ? acc[kN] + (uint64_t)(int64_t)o.body_add * kDelta
+                                              : (uint64_t)0 - acc[kN - j]);
+      out[j] = v;
+    }
+  } else {
+    uint64_t* dv = a.pool + (size_t)o.slot_a * S;
+    uint64_t* dh = a.pool + (size_t)o.slot_b * S;
+    uint64_t* sdv = o.snap_dv == kNoSlot ? nullptr : a.pool + (size_t)o.snap_dv * S;
+    uint64_t* sdh = o.snap_dh == kNoSlot ? nullptr : a.pool + (size_t)o.snap_dh * S;
+    for (uint32_t j = t; j <= kN; j += 128) {
+      const uint64_t step = j == 0 ? acc[0] : (j == kN ? acc[kN] : (uint64_t)0 - acc[kN - j]);
+      const uint64_t v_in = dv[j], h_in = dh[j];
+      const uint64_t v_out = step - h_in, h_out = step - v_in;
+      dv[j] = v_out;
+      dh[j] = h_out;
+      if (sdv) sdv[j] = v_out;
+      if (sdh) sdh[j] = h_out;
+    }
+  }
+}
+
+size_t blind_rotate_smem_bytes(uint32_t n) {
+  return 2 * kN * 8 + 2 * kM * 16 + ((n + 1) * 2 + 15) / 16 * 16;
+}
+
+// ------------------------------------------------------------------ KS
+// Key switch (big key kN -> small key n) fused with the linear prologue
+// (input = sum_q coef_q * pool[slot_q] + body_const * Delta) and the
+// modulus switch to 2N. Tile: KS_ITEMS items x 128 output coefficients per
+// CTA; the items' digits for a chunk of 32 input coefficients are staged in
+// shared memory and every KSK element loaded is reused across the tile.
+constexpr int KS_ITEMS = 16;
+constexpr int KS_CHUNK = 32;
+
+__device__ __forceinline__ uint64_t lin_coef(const LinDesc& d, const uint64_t* pool,
+                                             uint32_t stride, uint32_t j) {
+  uint64_t v = 0;
+  for (int q = 0; q < d.nterms; ++q)
+    v += (uint64_t)(int64_t)d.coef[q] * pool[(size_t)d.slot[q] * stride + j];
+  if (j == kBig) v += (uint64_t)(int64_t)d.body_const * kDelta;
+  return v;
+}
+
+__global__ void __launch_bounds__(128)
+keyswitch_kernel(KsArgs a) {
+  __shared__ int8_t dig[KS_ITEMS][KS_CHUNK][kKsLevel];
+  __shared__ LinDesc desc[KS_ITEMS];
+  const uint32_t t = threadIdx.x;
+  const uint32_t c = blockIdx.x * 128 + t;  // output coefficient
+  const uint32_t item0 = blockIdx.y * KS_ITEMS;
+  const uint32_t n = a.n;
+  const uint32_t row = n + 1;
+  if (t < KS_ITEMS) {
+    LinDesc d{};
+    if (item0 + t < a.count) d = a.desc[item0 + t];
+    desc[t] = d;
+  }
+  __syncthreads();
+
+  uint64_t acc[KS_ITEMS];
+#pragma unroll
+  for (int it = 0; it < KS_ITEMS; ++it) acc[it] = 0;
+
+  for (uint32_t j0 = 0; j0 < kBig; j0 += KS_CHUNK) {
+    __syncthreads();
+    for (uint32_t e = t; e < KS_ITEMS * KS_CHUNK; e += 128) {
+      const uint32_t it = e / KS_CHUNK, jj = e % KS_CHUNK;
+      int64_t dd[kKsLevel];
+      const uint64_t v = (item0 + it < a.count) ? lin_coef(desc[it], a.pool, a.pool_stride, j0 + jj) : 0;
+      decomp<kKsLevel>(v, kKsBaseLog, dd);
+#pragma unroll
+      for (int l = 0; l < (int)kKsLevel; ++l) dig[it][jj][l] = (int8_t)dd[l];
+    }
+    __syncthreads();
+    if (c < row) {
+      for (uint32_t jj = 0; jj < KS_CHUNK; ++jj) {
+#pragma unroll
+        for (int l = 0; l < (int)kKsLevel; ++l) {
+          const uint64_t kv = __ldg(a.ksk + ((size_t)(j0 + jj) * kKsLevel + l) * row + c);
+#pragma unroll
+          for (int it = 0; it < KS_ITEMS; ++it)
+            acc[it] -= (uint64_t)(int64_t)dig[it][jj][l] * kv;
+        }
+      }
+    }
+  }
+  if (c >= row) return;
+#pragma unroll
+  for (int it = 0; it < KS_ITEMS; ++it) {
+    const uint32_t item = item0 + it;
+    if (item >= a.count) break;
+    uint64_t v = acc[it];
+    if (c == n) v += lin_coef(desc[it], a.pool, a.pool_stride, kBig);
+    if (a.small_out) a.small_out[(size_t)item * row + c] = v;
+    a.ms[(size_t)item * a.ms_stride + c] = (uint16_t)modswitch(v);
+  }
+}
+
+// ------------------------------------------------------------------ linear
+// out[slot_out] = sum_q coef_q * pool[slot_q] + body_const * Delta.
+// Outputs may alias inputs only when every item reads the slots it writes
+// (the cell epilogue): each thread reads all its terms before writing.
+__global__ void linear_kernel(LinArgs a) {
+  const uint32_t item = blockIdx.y;
+  if (item >= a.count) return;
+  const LinOut& o = a.ops[item];
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= kBig; j += gridDim.x * blockDim.x) {
+    uint64_t v[LinOut::kMaxOut];
+#pragma unroll
+    for (int k = 0; k < LinOut::kMaxOut; ++k) {
+      if (k >= o.nout) break;
+      v[k] = lin_coef(o.d[k], a.pool, a.pool_stride, j);
+    }
+#pragma unroll
+    for (int k = 0; k < LinOut::kMaxOut; ++k) {
+      if (k >= o.nout) break;
+      a.pool[(size_t)o.out_slot[k] * a.pool_stride + j] = v[k];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ enc / phase
+__global__ void encrypt_kernel(EncArgs a) {
+  __shared__ uint64_t red[256];
+  const uint32_t item = blockIdx.x;
+  const uint64_t ctr = a.counter0 + item;
+  uint64_t* out = a.pool + (size_t)a.slots[item] * a.pool_stride;
+  uint64_t s = 0;
+  for (uint32_t j = threadIdx.x; j < kBig; j += blockDim.x) {
+    const uint64_t m = a.trivial ? 0 : philox_u64(a.seed, kDomEncMask, ctr * kBig + j);
+    out[j] = m;
+    if (a.sk_glwe[j]) s += m;
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (uint32_t w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    uint64_t b = a.trivial ? 0 : red[0] + (uint64_t)tuniform(a.seed, kDomEncNoise, ctr, a.noise_log2);
+    b += (uint64_t)(int64_t)a.values[item] * kDelta;
+    out[kBig] = b;
+  }
+}
+
+__global__ void phase_kernel(PhaseArgs a) {
+  __shared__ uint64_t red[256];
+  const uint32_t item = blockIdx.x;
+  const uint64_t* ct = a.pool + (size_t)a.slots[item] * a.pool_stride;
+  uint64_t s = 0;
+  for (uint32_t j = threadIdx.x; j < kBig; j += blockDim.x)
+    if (a.sk_glwe[j]) s += ct[j];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (uint32_t w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.phase[item] = ct[kBig] - red[0];
+}
+
+// ------------------------------------------------------------------ keygen
+__global__ void keygen_secret_kernel(uint64_t seed, uint32_t n, uint8_t* sk_small,
+                                     uint8_t* sk_glwe) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) sk_small[i] = (uint8_t)(philox_u64(seed, kDomSkSmall, i) & 1);
+  if (i < kBig) sk_glwe[i] = (uint8_t)(philox_u64(seed, kDomSkGlwe, i) & 1);
+}
+
+// One CTA per KSK row (j, l): LWE_s(s'_j * q / B^{l+1}).
+__global__ void keygen_ksk_kernel(uint64_t seed, uint32_t n, uint32_t noise_log2,
+                                  const uint8_t* sk_small, const uint8_t* sk_glwe,
+                                  uint64_t* ksk) {
+  __shared__ uint64_t red[256];
+  const uint32_t rowi = blockIdx.x;  // j * L + l
+  const uint32_t j = rowi / kKsLevel, l = rowi % kKsLevel;
+  uint64_t* row = ksk + (size_t)rowi * (n + 1);
+  uint64_t s = 0;
+  for (uint32_t c = threadIdx.x; c < n; c += blockDim.x) {
+    const uint64_t m = philox_u64(seed, kDomKskMask, (uint64_t)rowi * n + c);
+    row[c] = m;
+    if (sk_small[c]) s += m;
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (uint32_t w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    uint64_t b = red[0] + (uint64_t)tuniform(seed, kDomKskNoise, rowi, noise_log2);
+    if (sk_glwe[j]) b += 1ull << (64 - kKsBaseLog * (l + 1));
+    row[n] = b;
+  }
+}
+
+// One CTA (256 threads) per GGSW row (i, r): GLWE_S(0) + s_i * g on component r.
+// Output in the standard domain: bsk[((i*rows + r)*(k+1) + o)*N + c].
+__global__ void keygen_bsk_kernel(uint64_t seed, uint32_t noise_log2, const uint8_t* sk_small,
+                                  const uint8_t* sk_glwe, uint64_t* bsk) {
+  __shared__ uint64_t A[kN];
+  __shared__ uint8_t S[kN];
+  const uint32_t i = blockIdx.x / kRows, r = blockIdx.x % kRows;
+  const uint64_t rowi = (uint64_t)i * kRows + r;
+  for (uint32_t c = threadIdx.x; c < kN; c += blockDim.x) {
+    A[c] = philox_u64(seed, kDomBskMask, (rowi * kK + 0) * kN + c);
+    S[c] = sk_glwe[c];
+  }
+  __syncthreads();
+  uint64_t* mask = bsk + (rowi * (kK + 1) + 0) * kN;
+  uint64_t* body = bsk + (rowi * (kK + 1) + kK) * kN;
+  const uint32_t comp = r / kPbsLevel, lev = r % kPbsLevel + 1;
+  const uint64_t g = 1ull << (64 - kPbsBaseLog * lev);
+  const bool bit = sk_small[i] != 0;
+  for (uint32_t c = threadIdx.x; c < kN; c += blockDim.x) {
+    uint64_t b = (uint64_t)tuniform(seed, kDomBskNoise, rowi * kN + c, noise_log2);
+    // (A * S)_c = sum_t S_t * A_{c-t} (negacyclic)
+    for (uint32_t tt = 0; tt <= c; ++tt)
+      if (S[tt]) b += A[c - tt];
+    for (uint32_t tt = c + 1; tt < kN; ++tt)
+      if (S[tt]) b -= A[c + kN - tt];
+    uint64_t m = A[c];
+    if (bit && c == 0) {
+      if (comp == 0) m += g;
+      else b += g;
+    }
+    mask[c] = m;
+    body[c] = b;
+  }
+}
+
+// Fourier BSK: one CTA (128 threads) per GGSW row (i, r), both output
+// components transformed in lockstep with the same fft_forward the blind
+// rotation uses, then stored in the MAC layout [i][q*4 + r*2 + o][t].
+__global__ void __launch_bounds__(128)
+bsk_fourier_kernel(const uint64_t* bsk, const double2* __restrict__ tw,
+                   const double2* __restrict__ twist, double2* bskf) {
+  __shared__ double2 buf[2 * kM];
+  const uint32_t t = threadIdx.x;
+  const uint32_t i = blockIdx.x / kRows, r = blockIdx.x % kRows;
+  const uint64_t rowi = (uint64_t)i * kRows + r;
+  double2 X[2][8];
+#pragma unroll
+  for (int o = 0; o < 2; ++o) {
+    const uint64_t* poly = bsk + (rowi * (kK + 1) + o) * kN;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t x = t + 128 * q;
+      const double re = (double)(int64_t)poly[x];
+      const double im = (double)(int64_t)poly[x + kM];
+      X[o][q] = cmul(make_double2(re, im), __ldg(twist + x));
+    }
+  }
+  fft_forward<2>(X, buf, tw, t);
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+#pragma unroll
+    for (int o = 0; o < 2; ++o)
+      bskf[(size_t)i * (32 * 128) + (q * 4 + r * 2 + o) * 128 + t] = X[o][q];
+}
+
+// Debug / parity entry: forward transform of one integer polynomial, output
+// in natural spectrum order (bin f = 8t + q), for comparison with the oracle.
+__global__ void __launch_bounds__(128)
+fft_forward_debug_kernel(const int64_t* poly, const double2* __restrict__ tw,
+                         const double2* __restrict__ twist, double2* spec) {
+  __shared__ double2 buf[kM];
+  const uint32_t t = threadIdx.x;
+  double2 X[1][8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t x = t + 128 * q;
+    X[0][q] = cmul(make_double2((double)poly[x], (double)poly[x + kM]), __ldg(twist + x));
+  }
+  fft_forward<1>(X, buf, tw, t);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) spec[8 * t + q] = X[0][q];
+}
+
+__global__ void __launch_bounds__(128)
+fft_backward_debug_kernel(const double2* spec, const double2* __restrict__ tw,
+                          const double2* __restrict__ twist, uint64_t* poly) {
+  __shared__ double2 buf[kM];
+  const uint32_t t = threadIdx.x;
+  double2 X[1][8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) X[0][q] = spec[8 * t + q];
+  __syncthreads();
+  fft_inverse<1>(X, buf, tw, t);
+  const uint32_t h = (t >> 4) & 1, u = 16 * (t >> 5) + (t & 15);
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      const uint32_t x = u + 64 * (4 * h + q) + 512 * hi;
+      const double2 tv = __ldg(twist + x);
+      const double2 ut = make_double2(__dmul_rn(tv.x, 0x1p-10), __dmul_rn(-tv.y, 0x1p-10));
+      const double2 z = cmul(X[0][4 * hi + q], ut);
+      poly[x] = f64_to_torus(z.x);
+      poly[x + kM] = f64_to_torus(z.y);
+    }
+}
+
+}  // namespace lvb

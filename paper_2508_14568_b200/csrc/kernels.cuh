@@ -1,0 +1,120 @@
+// Kernel argument structs and launch wrappers (host <-> device contract).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace lvb {
+
+// A linear combination of pool ciphertexts plus a public constant:
+//   sum_q coef[q] * pool[slot[q]] + body_const * Delta.
+// Covers add/sub/scalar_mul/scalar_add/trivial and the fused prologues
+// (key = 3 dh - dv + eq9 + 4, fold z = 2x - 2y - eq + 1, ...).
+struct LinDesc {
+  uint32_t slot[4];
+  int32_t coef[4];
+  int32_t nterms;
+  int32_t body_const;
+};
+
+struct LinOut {
+  static constexpr int kMaxOut = 2;
+  LinDesc d[kMaxOut];
+  uint32_t out_slot[kMaxOut];
+  int32_t nout;
+};
+
+// Blind-rotation epilogue of one item.
+//   mode 0: pool[slot_a] = extract + body_add * Delta
+//   mode 1: Leuvenshtein cell (kernel.cpp:159-162), in place on the frontier:
+//           dv = pool[slot_a], dh = pool[slot_b] (read first), then
+//           pool[slot_a] = step - dh, pool[slot_b] = step - dv, with optional
+//           snapshots of the new dv / dh into snap_dv / snap_dh (~0u = none).
+struct BrOut {
+  uint32_t mode;
+  uint32_t slot_a;
+  uint32_t slot_b;
+  uint32_t snap_dv;
+  uint32_t snap_dh;
+  int32_t body_add;
+};
+constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
+
+struct BrArgs {
+  const uint16_t* ms;          // [count][ms_stride] modulus-switched small LWE
+  uint32_t ms_stride;
+  const uint32_t* lut_of_item; // [count] test polynomial index
+  const uint64_t* test_polys;  // [luts][N]
+  const double2* bskf;         // Fourier BSK, MAC layout
+  const double2* twiddles;     // W[t], t < kM/2
+  const double2* twist;        // zeta^j, j < kM
+  uint32_t n;
+  uint64_t* pool;              // pool base
+  uint32_t pool_stride;
+  const BrOut* outs;           // [count]
+};
+
+struct KsArgs {
+  const LinDesc* desc;  // [count]
+  const uint64_t* pool;
+  uint32_t pool_stride;
+  const uint64_t* ksk;  // [kN][ks_level][n+1]
+  uint32_t n;
+  uint32_t count;
+  uint16_t* ms;         // [count][ms_stride]
+  uint32_t ms_stride;
+  uint64_t* small_out;  // optional [count][n+1] (parity/debug)
+};
+
+struct LinArgs {
+  const LinOut* ops;
+  uint64_t* pool;
+  uint32_t pool_stride;
+  uint32_t count;
+};
+
+struct EncArgs {
+  uint64_t* pool;
+  uint32_t pool_stride;
+  const uint32_t* slots;
+  const int32_t* values;
+  const uint8_t* sk_glwe;
+  uint64_t seed;
+  uint64_t counter0;
+  uint32_t noise_log2;
+  int trivial;
+};
+
+struct PhaseArgs {
+  const uint64_t* pool;
+  uint32_t pool_stride;
+  const uint32_t* slots;
+  const uint8_t* sk_glwe;
+  uint64_t* phase;
+};
+
+__global__ void blind_rotate_kernel(BrArgs a);
+size_t blind_rotate_smem_bytes(uint32_t n);
+__global__ void keyswitch_kernel(KsArgs a);
+__global__ void linear_kernel(LinArgs a);
+__global__ void encrypt_kernel(EncArgs a);
+__global__ void phase_kernel(PhaseArgs a);
+__global__ void keygen_secret_kernel(uint64_t seed, uint32_t n, uint8_t* sk_small, uint8_t* sk_glwe);
+__global__ void keygen_ksk_kernel(uint64_t seed, uint32_t n, uint32_t noise_log2,
+                                  const uint8_t* sk_small, const uint8_t* sk_glwe, uint64_t* ksk);
+__global__ void keygen_bsk_kernel(uint64_t seed, uint32_t noise_log2, const uint8_t* sk_small,
+                                  const uint8_t* sk_glwe, uint64_t* bsk);
+__global__ void bsk_fourier_kernel(const uint64_t* bsk, const double2* tw, const double2* twist,
+                                   double2* bskf);
+__global__ void fft_forward_debug_kernel(const int64_t* poly, const double2* tw,
+                                         const double2* twist, double2* spec);
+__global__ void fft_backward_debug_kernel(const double2* spec, const double2* tw,
+                                          const double2* twist, uint64_t* poly);
+
+constexpr int kKsItems = 16;
+
+}  // namespace lvb

@@ -1,0 +1,527 @@
+// Anti-diagonal wavefront scheduler: the B200 form of kernel::distance
+// (proj/src/kernel.cpp:209-259), distance_encrypted (:261-268),
+// preprocess::build_eq_table / distance_preprocessed
+// (proj/src/preprocess.cpp:38-76).
+//
+// The reference visits one cell at a time. Every cell on an anti-diagonal
+// is independent, and so is every stage-s equality check of
+// every (i, j) pair, so one launch ("wave") carries
+//   - the cell bootstraps of diagonal k            (key -> min table)
+//   - equality stage S-1 of diagonal k+1            (-> eq_lut(9))
+//   - ...
+//   - equality stage 0 of diagonal k+S              (-> eq_lut(1) or (9))
+// for every pair of a batch. Refreshes chosen by the symbolic ledger plan
+// (ledger.cpp) run as a sub-wave in front of the cells that need them.
+// All wave descriptors are built once on the host and uploaded in one copy;
+// the waves are then replayed on the stream (captured as a CUDA graph).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "context.hpp"
+
+namespace lvb {
+
+extern thread_local std::string g_last_error;
+std::array<int32_t, 16> eq_lut_entries(int scale);
+
+template <typename F>
+static int guard_wf(F&& f) {
+  try {
+    f();
+    return LV_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return LV_ERR_CUDA;
+  }
+}
+
+static BandSpec to_band(const lv_band* b) {
+  BandSpec s;
+  s.mode = b->mode;
+  s.half_width = b->half_width;
+  return s;
+}
+
+static const PairPlan& get_plan(lv_ctx* c, uint32_t m, uint32_t n, const BandSpec& band,
+                                bool negated, double budget) {
+  if (!band.covers(m, n))
+    throw Error(LV_ERR_BAND_TOO_NARROW, "band half-width " + std::to_string(band.half_width) +
+                                            " below length difference");
+  if (budget < 11.0)  // kernel.cpp:18, 216-218
+    throw Error(LV_ERR_INVALID_PARAMS, "noise budget below 11: refreshed operands alone exceed it");
+  const std::string key = std::to_string(m) + "/" + std::to_string(n) + "/" +
+                          std::to_string(band.mode) + "/" + std::to_string(band.half_width) + "/" +
+                          (negated ? "n" : "o") + "/" + std::to_string(budget);
+  auto it = c->plan_cache.find(key);
+  if (it != c->plan_cache.end()) return it->second;
+  return c->plan_cache.emplace(key, plan_pair(m, n, band, negated, budget)).first->second;
+}
+
+// One pair's traversal inputs.
+struct PairIn {
+  uint32_t m, n;
+  BandSpec band;
+  const lv_ct* a;  // m * S symbol handles (ee) / unused (pre)
+  const lv_ct* b;  // n * S symbol handles (ee)
+  const lv_eqtable* table = nullptr;
+  const char* plain = nullptr;
+};
+
+struct Wave {
+  std::vector<PbsItem> pre;   // refresh sub-wave
+  std::vector<PbsItem> main;  // equality stages + cells
+};
+
+static LinDesc lin(std::initializer_list<std::pair<uint32_t, int32_t>> terms, int32_t body) {
+  LinDesc d{};
+  int q = 0;
+  for (const auto& t : terms) {
+    d.slot[q] = t.first;
+    d.coef[q] = t.second;
+    ++q;
+  }
+  d.nterms = q;
+  d.body_const = body;
+  return d;
+}
+
+// Runs a batch of traversals (S = symbols per character; S == 0 selects
+// the preprocessed mode with eq9 taken from the pair's table).
+static void run_traversals(lv_ctx* c, const std::vector<PairIn>& pairs, uint32_t S, bool negated,
+                           lv_ct* scores, lv_run* runs) {
+  const double budget = c->p.max_variance_budget;
+  const uint32_t lut_min = c->min_lut[negated ? 1 : 0];
+  uint32_t lut_eq1 = 0, lut_eq9 = 0;
+  if (S > 0) {
+    lut_eq1 = lut_id(c, eq_lut_entries(1));
+    lut_eq9 = lut_id(c, eq_lut_entries(9));
+  }
+  const int32_t dv_coef = negated ? -1 : 1;
+
+  std::vector<const PairPlan*> plans(pairs.size());
+  for (size_t p = 0; p < pairs.size(); ++p) {
+    const PairIn& in = pairs[p];
+    plans[p] = &get_plan(c, in.m, in.n, in.band, negated, budget);
+    if (in.table) {
+      for (uint32_t j = 0; j < in.n; ++j)
+        if (!in.table->rows.count(in.plain[j]))
+          throw Error(LV_ERR_CHAR_NOT_IN_SUBSET,
+                      std::string("no table row for character '") + in.plain[j] + "'");
+      if (in.table->length != in.m) throw Error(LV_ERR_INVALID_PARAMS, "table length mismatch");
+    }
+  }
+
+  // frontier slots (index 0 unused), initialised to trivial(1)
+  std::vector<std::vector<lv_ct>> vrow(pairs.size()), hcol(pairs.size());
+  std::vector<lv_ct> all_frontier;
+  for (size_t p = 0; p < pairs.size(); ++p) {
+    vrow[p] = pool_alloc(c, pairs[p].m + 1);
+    hcol[p] = pool_alloc(c, pairs[p].n + 1);
+    all_frontier.insert(all_frontier.end(), vrow[p].begin(), vrow[p].end());
+    all_frontier.insert(all_frontier.end(), hcol[p].begin(), hcol[p].end());
+  }
+  {
+    std::vector<int32_t> ones(all_frontier.size(), 1);
+    if (!all_frontier.empty()) {
+      uint32_t* ds = c->u32a.get(all_frontier.size());
+      int32_t* dv = c->i32a.get(all_frontier.size());
+      LV_CUDA(cudaMemcpyAsync(ds, all_frontier.data(), all_frontier.size() * 4,
+                              cudaMemcpyHostToDevice, c->stream));
+      LV_CUDA(cudaMemcpyAsync(dv, ones.data(), ones.size() * 4, cudaMemcpyHostToDevice, c->stream));
+      EncArgs ea{c->d_pool, kBigStride, ds, dv, c->d_sk_glwe, c->seed, 0, 0, 1};
+      encrypt_kernel<<<(uint32_t)all_frontier.size(), 256, 0, c->stream>>>(ea);
+      LV_CUDA(cudaGetLastError());
+    }
+  }
+
+  // score path: trivial reads count as a constant, stored cells need a
+  // slot (final frontier for the exact band's last row, else a snapshot).
+  std::vector<std::vector<lv_ct>> path_slots(pairs.size());
+  std::vector<int32_t> path_const(pairs.size(), 0);
+  std::vector<std::map<uint64_t, uint32_t>> snap_v(pairs.size()), snap_h(pairs.size());
+  std::vector<lv_ct> snapshots;
+  for (size_t p = 0; p < pairs.size(); ++p) {
+    const PairIn& in = pairs[p];
+    for (const PathRead& r : plans[p]->path) {
+      const bool boundary = r.vertical ? r.j == 0 : r.i == 0;
+      if (boundary || !in.band.in_band(r.i, r.j)) {
+        path_const[p] += 1;
+        continue;
+      }
+      if (in.band.mode == BandSpec::exact && !r.vertical && r.i == in.m) {
+        path_slots[p].push_back(hcol[p][r.j]);
+        continue;
+      }
+      const lv_ct s = pool_alloc(c, 1)[0];
+      snapshots.push_back(s);
+      path_slots[p].push_back(s);
+      (r.vertical ? snap_v : snap_h)[p][((uint64_t)r.i << 32) | r.j] = s;
+    }
+  }
+
+  // build the waves
+  std::map<int64_t, Wave> waves;
+  std::vector<lv_ct> temps;
+  uint64_t eq_pbs_total = 0, linear_ops = 0;
+  for (size_t p = 0; p < pairs.size(); ++p) {
+    const PairIn& in = pairs[p];
+    const PairPlan& plan = *plans[p];
+    lv_run r{};
+    for (const CellPlan& cell : plan.cells) {
+      const int64_t k = (int64_t)cell.i + cell.j;
+      const int64_t wcell = k - 2 + S;
+      lv_ct eq9;
+      if (S > 0) {
+        const lv_ct* ai = in.a + (size_t)(cell.i - 1) * S;
+        const lv_ct* bj = in.b + (size_t)(cell.j - 1) * S;
+        std::vector<lv_ct> eqs = pool_alloc(c, S);
+        temps.insert(temps.end(), eqs.begin(), eqs.end());
+        for (uint32_t s = 0; s < S; ++s) {
+          PbsItem it{};
+          if (s == 0)
+            it.in = lin({{ai[0], 1}, {bj[0], -1}}, 0);  // eq4: sub(x, y)
+          else  // fold_step: 2 (x_s - y_s) + (1 - eq_prev)
+            it.in = lin({{ai[s], 2}, {bj[s], -2}, {eqs[s - 1], -1}}, 1);
+          it.lut = (s + 1 == S) ? lut_eq9 : lut_eq1;
+          it.out = BrOut{0, eqs[s], kNoSlot, kNoSlot, kNoSlot, 0};
+          waves[k - 2 + s].main.push_back(it);
+        }
+        eq9 = eqs[S - 1];
+        r.equality_pbs += S;
+        linear_ops += 1 + 4 * (S - 1);
+      } else {
+        eq9 = in.table->rows.at(in.plain[cell.j - 1])[cell.i - 1];
+      }
+      const lv_ct dv = vrow[p][cell.i], dh = hcol[p][cell.j];
+      Wave& w = waves[wcell];
+      if (cell.refresh_dv) {  // kernel.cpp:183-188: refresh(dv + 1) - 1
+        PbsItem it{};
+        it.in = lin({{dv, 1}}, 1);
+        it.lut = c->identity_lut;
+        it.out = BrOut{0, dv, kNoSlot, kNoSlot, kNoSlot, -1};
+        w.pre.push_back(it);
+        linear_ops += 2;
+      }
+      if (cell.refresh_dh) {
+        PbsItem it{};
+        it.in = lin({{dh, 1}}, 1);
+        it.lut = c->identity_lut;
+        it.out = BrOut{0, dh, kNoSlot, kNoSlot, kNoSlot, -1};
+        w.pre.push_back(it);
+        linear_ops += 2;
+      }
+      PbsItem it{};
+      // cell_kernel key (kernel.cpp:152-158): negated 3 dh - dv + eq9 + 4,
+      // original dv + 3 dh + eq9 + 4
+      it.in = lin({{dv, dv_coef}, {dh, 3}, {eq9, 1}}, 4);
+      it.lut = lut_min;
+      const uint64_t key = ((uint64_t)cell.i << 32) | cell.j;
+      auto sv = snap_v[p].find(key);
+      auto sh = snap_h[p].find(key);
+      it.out = BrOut{1, dv, dh, sv == snap_v[p].end() ? kNoSlot : sv->second,
+                     sh == snap_h[p].end() ? kNoSlot : sh->second, 0};
+      w.main.push_back(it);
+      linear_ops += 6;
+      r.kernel_pbs += 1;
+      r.visited_cells += 1;
+    }
+    r.refreshes = plan.refreshes;
+    r.max_key_variance = plan.max_key_variance;
+    linear_ops += plan.path.size();
+    eq_pbs_total += r.equality_pbs;
+    runs[p] = r;
+  }
+
+  // flatten + single upload
+  std::vector<LinDesc> d;
+  std::vector<uint32_t> l;
+  std::vector<BrOut> o;
+  struct Launch {
+    size_t off, count;
+  };
+  std::vector<Launch> launches;
+  uint64_t total_items = 0;
+  for (auto& kv : waves) {
+    for (auto* part : {&kv.second.pre, &kv.second.main}) {
+      if (part->empty()) continue;
+      launches.push_back({d.size(), part->size()});
+      for (const PbsItem& it : *part) {
+        d.push_back(it.in);
+        l.push_back(it.lut);
+        o.push_back(it.out);
+      }
+      total_items += part->size();
+    }
+  }
+  if (!d.empty()) {
+    LinDesc* dd = c->desc.get(d.size());
+    uint32_t* dl = c->lut_item.get(l.size());
+    BrOut* dout = c->br_out.get(o.size());
+    LV_CUDA(cudaMemcpyAsync(dd, d.data(), d.size() * sizeof(LinDesc), cudaMemcpyHostToDevice, c->stream));
+    LV_CUDA(cudaMemcpyAsync(dl, l.data(), l.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    LV_CUDA(cudaMemcpyAsync(dout, o.data(), o.size() * sizeof(BrOut), cudaMemcpyHostToDevice, c->stream));
+    size_t max_wave = 0;
+    for (const Launch& L : launches) max_wave = std::max(max_wave, L.count);
+    c->ms.get(max_wave * ms_stride(c));  // size scratch before capture
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    LV_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    for (const Launch& L : launches)
+      launch_pbs_dev(c, dd + L.off, dl + L.off, dout + L.off, (uint32_t)L.count);
+    LV_CUDA(cudaStreamEndCapture(c->stream, &graph));
+    LV_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    LV_CUDA(cudaGraphLaunch(exec, c->stream));
+    LV_CUDA(cudaStreamSynchronize(c->stream));
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+  }
+
+  // score = trivial(0) + sum of path reads (kernel.cpp:193-200)
+  std::vector<lv_ct> outs = pool_alloc(c, pairs.size());
+  std::vector<LinOut> sum_ops;
+  for (size_t p = 0; p < pairs.size(); ++p) {
+    // chain of <=4-term linear combinations accumulating into outs[p]
+    const auto& ps = path_slots[p];
+    size_t q = 0;
+    bool first = true;
+    do {
+      LinOut op{};
+      op.nout = 1;
+      op.out_slot[0] = outs[p];
+      LinDesc dsc{};
+      int t = 0;
+      if (!first) {
+        dsc.slot[t] = outs[p];
+        dsc.coef[t] = 1;
+        ++t;
+      }
+      while (t < 4 && q < ps.size()) {
+        dsc.slot[t] = ps[q++];
+        dsc.coef[t] = 1;
+        ++t;
+      }
+      dsc.nterms = t;
+      dsc.body_const = first ? path_const[p] : 0;
+      op.d[0] = dsc;
+      sum_ops.push_back(op);
+      first = false;
+    } while (q < ps.size());
+  }
+  // the chain for one pair is sequential; issue level by level
+  {
+    std::vector<std::vector<LinOut>> levels;
+    std::vector<size_t> lvl_of(pairs.size(), 0);
+    size_t idx = 0;
+    for (size_t p = 0; p < pairs.size(); ++p) {
+      const auto& ps = path_slots[p];
+      const size_t steps = ps.size() <= 4 ? 1 : 1 + (ps.size() - 4 + 2) / 3;
+      for (size_t s = 0; s < steps; ++s) {
+        if (levels.size() <= s) levels.resize(s + 1);
+        levels[s].push_back(sum_ops[idx++]);
+      }
+    }
+    for (auto& lv : levels) run_linear(c, lv);
+  }
+
+  // ledgers, counters, cleanup
+  for (size_t p = 0; p < pairs.size(); ++p) {
+    NoiseLedger led;
+    for (int32_t coef : plans[p]->score_coeffs) {
+      NoiseLedger one = NoiseLedger::fresh(c->next_source++);
+      led.add_scaled(one, coef);
+    }
+    c->ledgers[outs[p]] = std::move(led);
+    scores[p] = outs[p];
+    runs[p].waves = waves.size();
+  }
+  pool_free(c, all_frontier.data(), all_frontier.size());
+  pool_free(c, temps.data(), temps.size());
+  pool_free(c, snapshots.data(), snapshots.size());
+  uint64_t refreshes = 0;
+  for (size_t p = 0; p < pairs.size(); ++p) refreshes += runs[p].refreshes;
+  c->pbs_count += total_items;
+  c->refresh_count += refreshes;
+  c->linear_count += linear_ops;
+  (void)eq_pbs_total;
+}
+
+}  // namespace lvb
+
+using namespace lvb;
+
+extern "C" {
+
+int lv_band_resolve(int32_t mode, uint64_t ell, uint64_t m, uint64_t n, lv_band* out) {
+  return guard_wf([&] {
+    const uint64_t mx = std::max(m, n);
+    if (mode == LV_BAND_EXACT)
+      *out = lv_band{LV_BAND_EXACT, mx};
+    else if (mode == LV_BAND_SKIP)
+      *out = lv_band{LV_BAND_SKIP, (mx + 1) / 2};
+    else if (mode == LV_BAND_APPROX)
+      *out = lv_band{LV_BAND_APPROX, ell};
+    else
+      throw Error(LV_ERR_INVALID_PARAMS, "unknown band mode");
+  });
+}
+
+int lv_edit_distance_ee(lv_ctx* c, const lv_ct* a, size_t m, const lv_ct* b, size_t n,
+                        uint32_t symbols, const lv_band* band, int32_t key_encoding, lv_ct* score,
+                        lv_run* run) {
+  return guard_wf([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (symbols < 1)
+      throw Error(LV_ERR_INVALID_PARAMS, "equality operands must have the same nonzero symbol count");
+    check_handles(c, a, m * symbols);
+    check_handles(c, b, n * symbols);
+    std::vector<PairIn> pairs{PairIn{(uint32_t)m, (uint32_t)n, to_band(band), a, b}};
+    run_traversals(c, pairs, symbols, key_encoding == LV_KEY_NEGATED, score, run);
+  });
+}
+
+int lv_edit_distance_batch(lv_ctx* c, size_t npairs, const lv_ct* a, const uint64_t* a_off,
+                           const lv_ct* b, const uint64_t* b_off, uint32_t symbols,
+                           const lv_band* bands, int32_t key_encoding, lv_ct* scores, lv_run* runs) {
+  return guard_wf([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (symbols < 1)
+      throw Error(LV_ERR_INVALID_PARAMS, "equality operands must have the same nonzero symbol count");
+    std::vector<PairIn> pairs;
+    for (size_t p = 0; p < npairs; ++p) {
+      const uint64_t m = a_off[p + 1] - a_off[p], n = b_off[p + 1] - b_off[p];
+      check_handles(c, a + a_off[p] * symbols, m * symbols);
+      check_handles(c, b + b_off[p] * symbols, n * symbols);
+      pairs.push_back(PairIn{(uint32_t)m, (uint32_t)n, to_band(&bands[p]), a + a_off[p] * symbols,
+                             b + b_off[p] * symbols});
+    }
+    run_traversals(c, pairs, symbols, key_encoding == LV_KEY_NEGATED, scores, runs);
+  });
+}
+
+int lv_eq_table_build(lv_ctx* c, const lv_ct* a, size_t m, uint32_t S, const char* chars,
+                      const int32_t* char_symbols, size_t rows, lv_eqtable** out,
+                      uint64_t* build_pbs) {
+  return guard_wf([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (S < 1)
+      throw Error(LV_ERR_INVALID_PARAMS, "equality operands must have the same nonzero symbol count");
+    check_handles(c, a, m * S);
+    const uint32_t lut_eq1 = lut_id(c, eq_lut_entries(1));
+    const uint32_t lut_eq9 = lut_id(c, eq_lut_entries(9));
+    auto* t = new lv_eqtable();
+    t->length = m;
+    try {
+      // stage-major waves over all (row, position) entries (preprocess.cpp:47-57)
+      std::vector<std::vector<lv_ct>> eqs(rows * m);
+      for (size_t e = 0; e < rows * m; ++e) eqs[e] = pool_alloc(c, S);
+      for (uint32_t s = 0; s < S; ++s) {
+        std::vector<PbsItem> items;
+        items.reserve(rows * m);
+        for (size_t r = 0; r < rows; ++r)
+          for (size_t i = 0; i < m; ++i) {
+            const lv_ct* ai = a + i * S;
+            const int32_t ys = char_symbols[r * S + s];
+            PbsItem it{};
+            if (s == 0)
+              it.in = lin({{ai[0], 1}}, -ys);
+            else
+              it.in = lin({{ai[s], 2}, {eqs[r * m + i][s - 1], -1}}, 1 - 2 * ys);
+            it.lut = (s + 1 == S) ? lut_eq9 : lut_eq1;
+            it.out = BrOut{0, eqs[r * m + i][s], kNoSlot, kNoSlot, kNoSlot, 0};
+            items.push_back(it);
+          }
+        run_pbs_items(c, items);
+      }
+      for (size_t r = 0; r < rows; ++r) {
+        std::vector<lv_ct> row(m);
+        for (size_t i = 0; i < m; ++i) {
+          row[i] = eqs[r * m + i][S - 1];
+          c->ledgers[row[i]] = NoiseLedger::fresh(c->next_source++);
+          if (S > 1) pool_free(c, eqs[r * m + i].data(), S - 1);
+        }
+        if (t->rows.count(chars[r])) pool_free(c, t->rows[chars[r]].data(), m);
+        t->rows[chars[r]] = std::move(row);
+      }
+      const uint64_t pbs = (uint64_t)rows * m * S;
+      c->pbs_count += pbs;
+      c->linear_count += (uint64_t)rows * m * (1 + 4 * (S - 1));
+      if (build_pbs) *build_pbs = pbs;
+    } catch (...) {
+      delete t;
+      throw;
+    }
+    *out = t;
+  });
+}
+
+int lv_eq_table_lookup(lv_ctx* c, const lv_eqtable* t, char ch, uint64_t position, lv_ct* out) {
+  return guard_wf([&] {
+    (void)c;
+    auto it = t->rows.find(ch);
+    if (it == t->rows.end())  // preprocess.cpp:21-31
+      throw Error(LV_ERR_CHAR_NOT_IN_SUBSET, std::string("no table row for character '") + ch + "'");
+    if (position < 1 || position > t->length)
+      throw Error(LV_ERR_POSITION_OUT_OF_RANGE, "position " + std::to_string(position) +
+                                                    " outside 1.." + std::to_string(t->length));
+    *out = it->second[position - 1];
+  });
+}
+
+void lv_eq_table_destroy(lv_ctx* c, lv_eqtable* t) {
+  if (!t) return;
+  if (c) {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    for (auto& kv : t->rows) pool_free(c, kv.second.data(), kv.second.size());
+  }
+  delete t;
+}
+
+int lv_edit_distance_pre(lv_ctx* c, const lv_eqtable* t, const char* plain, size_t n,
+                         const lv_band* band, int32_t key_encoding, lv_ct* score, lv_run* run) {
+  return guard_wf([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    PairIn in{(uint32_t)t->length, (uint32_t)n, to_band(band), nullptr, nullptr, t, plain};
+    std::vector<PairIn> pairs{in};
+    run_traversals(c, pairs, 0, key_encoding == LV_KEY_NEGATED, score, run);
+  });
+}
+
+int lv_plan_trace(uint64_t m, uint64_t n, const lv_band* band, int32_t key_encoding, double budget,
+                  uint64_t cap, uint32_t* ij, int64_t* key_var, uint32_t* refreshes,
+                  uint64_t* count, lv_run* totals) {
+  return guard_wf([&] {
+    const BandSpec b = to_band(band);
+    if (!b.covers(m, n))
+      throw Error(LV_ERR_BAND_TOO_NARROW,
+                  "band half-width " + std::to_string(b.half_width) + " below length difference");
+    if (budget < 11.0)
+      throw Error(LV_ERR_INVALID_PARAMS, "noise budget below 11: refreshed operands alone exceed it");
+    const PairPlan plan = plan_pair((uint32_t)m, (uint32_t)n, b, key_encoding == LV_KEY_NEGATED, budget);
+    const uint64_t k = plan.cells.size();
+    for (uint64_t q = 0; q < std::min(k, cap); ++q) {
+      ij[2 * q] = plan.cells[q].i;
+      ij[2 * q + 1] = plan.cells[q].j;
+      key_var[q] = plan.cells[q].key_variance;
+      refreshes[q] = plan.cells[q].refresh_dv + plan.cells[q].refresh_dh;
+    }
+    *count = k;
+    if (totals) {
+      lv_run r{};
+      r.visited_cells = k;
+      r.kernel_pbs = k;
+      r.refreshes = plan.refreshes;
+      r.max_key_variance = plan.max_key_variance;
+      *totals = r;
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+"""GPU parity of the PBS path against the CPU oracle, stage by stage, at the
+default (production) parameter set. Integer stages and the f64 FFT
+external product are required to be BIT-EXACT (the FFT operation order is
+specified in oracle/tfhe_oracle.c and reproduced by csrc/fft.cuh)."""
+import numpy as np
+import pytest
+
+import paper_2508_14568_b200 as L
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def test_keygen_bit_exact(ctx, orc):
+    sks, skg, ksk, bskf = ctx.debug_keys()
+    assert np.array_equal(sks, orc.sk_small())
+    assert np.array_equal(skg, orc.sk_glwe())
+    assert np.array_equal(ksk, orc.ksk())
+    assert np.array_equal(bskf.view(np.uint64), orc.bskf().view(np.uint64))
+
+
+def test_fft_bit_exact(ctx, orc):
+    rng = np.random.default_rng(11)
+    for scale in (2 ** 22, 2 ** 62):
+        p = rng.integers(-scale, scale, 2048)
+        spec, rt = ctx.debug_fft(p)
+        want = orc.fft_forward(p)
+        assert np.array_equal(spec.view(np.uint64), want.view(np.uint64))
+        assert np.array_equal(rt, orc.fft_backward(want))
+
+
+def test_encrypt_bit_exact_and_decrypts(golden):
+    c = L.Context(seed=0)
+    vals = list(range(32)) * 2
+    h = c.encrypt(vals)
+    rows = c.export(h)
+    o = O.Oracle(0)
+    for i, v in enumerate(vals):
+        assert np.array_equal(rows[i], o.encrypt(v, i))
+    assert list(c.decrypt(h)) == vals
+    c.close()
+
+
+def test_keyswitch_bit_exact(ctx, orc):
+    rows = np.stack([orc.encrypt(v, 1000 + v) for v in range(24)])
+    got = ctx.debug_keyswitch(rows)
+    for i in range(len(rows)):
+        assert np.array_equal(got[i], orc.keyswitch(rows[i]))
+
+
+def test_blind_rotate_bit_exact(ctx, orc, golden):
+    lut = np.array(golden["luts"]["minlut-negated"], np.int32)
+    lid = ctx.lut(lut)
+    rows = [orc.encrypt(v, 2000 + v) for v in range(6)]
+    ms = np.stack([orc.modswitch(orc.keyswitch(r)) for r in rows])
+    got = ctx.debug_blind_rotate(ms, [lid] * len(rows))
+    tp = orc.test_poly(lut)
+    for i in range(len(rows)):
+        want = orc.sample_extract(orc.blind_rotate(ms[i], tp))
+        assert np.array_equal(got[i], want)
+
+
+def test_pbs_bit_exact_all_luts(ctx, orc, golden):
+    names = ["identity", "minlut-negated", "minlut-original", "eqlut1", "eqlut9"]
+    luts = np.array([golden["luts"][n] for n in names], np.int32)
+    ids = np.array([ctx.lut(l) for l in luts], np.uint32)
+    xs = np.arange(40) % 32
+    rows = np.stack([orc.encrypt(int(x), 3000 + i) for i, x in enumerate(xs)])
+    which = np.arange(40) % len(names)
+    got = ctx.pbs_host(rows, ids[which])
+    want = orc.pbs_batch(rows, luts[which])
+    assert np.array_equal(got, want)
+    for i, x in enumerate(xs):
+        assert orc.decrypt(got[i]) == L.negacyclic_eval(luts[which[i]], int(x))
+
+
+def test_pbs_handles_budget_and_counters(golden):
+    c = L.Context(seed=5, budget=25.0)  # NoiseParams::tight(), backend.hpp:29
+    lut = [(x - 4 + 16) % 16 for x in range(16)]  # test_backend.cpp:16-24
+    out = c.pbs(c.encrypt([5]), lut)
+    assert list(c.decrypt(out)) == [1]
+    assert list(c.variance(out)) == [1]
+    assert c.stats()["pbs_count"] == 1
+    noisy = c.trivial([0])
+    for _ in range(25):
+        noisy = c.add(noisy, c.encrypt([0]))
+    assert list(c.variance(noisy)) == [25]
+    c.pbs(noisy, lut)
+    noisy = c.add(noisy, c.encrypt([0]))
+    with pytest.raises(L.NoiseBudgetExceeded):
+        c.pbs(noisy, lut)
+    seven = c.refresh(c.encrypt([7]))
+    assert list(c.decrypt(seven)) == [7]
+    with pytest.raises(L.ValueOutsideLutHalf):
+        c.refresh(c.encrypt([16]))
+    assert c.stats()["refresh_count"] == 1
+    with pytest.raises(L.OutOfRangeValue):
+        c.encrypt([32])
+    c.close()
+
+
+def test_linear_ops_follow_reference(ctx):
+    a = ctx.encrypt([3])
+    assert list(ctx.decrypt(ctx.scalar_mul(a, 3))) == [9]
+    assert list(ctx.variance(ctx.scalar_mul(a, 3))) == [9]
+    gone = ctx.sub(a, a)
+    assert list(ctx.decrypt(gone)) == [0] and list(ctx.variance(gone)) == [0]
+    assert list(ctx.decrypt(ctx.scalar_add(ctx.encrypt([30]), 5))) == [3]
+    assert list(ctx.decrypt(ctx.scalar_mul(ctx.encrypt([1]), -1))) == [31]
+    x, y = ctx.encrypt([1]), ctx.encrypt([2])
+    shared = ctx.sub(x, y)
+    assert ctx.predict_variance([(x[0], 1), (y[0], 3)]) == 10
+    assert ctx.predict_variance([(x[0], 1), (shared[0], 1)]) == 5
+
+
+def test_random_linear_circuits(ctx):
+    rng = np.random.default_rng(11)  # test_backend.cpp:67-110
+    for _ in range(20):
+        plain = list(rng.integers(0, 32, 4))
+        cts = list(ctx.encrypt(plain))
+        for _ in range(12):
+            i, j = rng.integers(0, len(cts), 2)
+            op = rng.integers(0, 4)
+            if op == 0:
+                cts.append(ctx.add([cts[i]], [cts[j]])[0]); plain.append((plain[i] + plain[j]) % 32)
+            elif op == 1:
+                cts.append(ctx.sub([cts[i]], [cts[j]])[0]); plain.append((plain[i] - plain[j]) % 32)
+            elif op == 2:
+                k = int(rng.integers(0, 7)) - 3
+                cts.append(ctx.scalar_mul([cts[i]], k)[0]); plain.append((plain[i] * k) % 32)
+            else:
+                k = int(rng.integers(0, 32))
+                cts.append(ctx.scalar_add([cts[i]], k)[0]); plain.append((plain[i] + k) % 32)
+        assert list(ctx.decrypt(cts)) == [int(p) for p in plain]

@@ -1,0 +1,79 @@
+"""GPU end to end: decrypted distances and every counter of
+cli::compute_report equal the reference's (tests/golden, produced by the
+reference's own SimBackend), through the wavefront scheduler."""
+import pytest
+
+import paper_2508_14568_b200 as L
+from paper_2508_14568_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+ERR = {"BandTooNarrow": L.BandTooNarrow, "CharNotInAlphabet": L.CharNotInAlphabet,
+       "InvalidParams": L.InvalidParams, "CharNotInSubset": L.CharNotInSubset}
+
+FIELDS = ["distance", "visited_cells", "pbs_total", "pbs_equality", "pbs_kernel", "refresh_count",
+          "preprocessing_pbs", "max_key_variance", "linear_ops", "half_width"]
+
+
+def run_case(case):
+    return L.compute(case["a"], case["b"], mode=case["mode"],
+                     ell=case["ell"] if case["mode"] == "approx" else None,
+                     encoding=case["encoding"], budget=case["budget"],
+                     key_encoding=case["key_encoding"], preprocess=case["preprocess"])
+
+
+def test_reference_cases(golden):
+    for case in golden["cases"]:
+        if "error" in case:
+            with pytest.raises(ERR[case["error"]]):
+                run_case(case)
+            continue
+        got = run_case(case)
+        want = case["report"]
+        for f in FIELDS:
+            assert got[f] == want[f], (case["a"], case["b"], f, got[f], want[f])
+
+
+def test_worked_examples():
+    r = L.compute("monday", "friday")  # test_kernel.cpp:230-249
+    assert (r["distance"], r["pbs_kernel"], r["pbs_equality"], r["refresh_count"]) == (3, 36, 72, 0)
+    assert L.compute("KID", "SIT")["distance"] == 2
+    assert L.compute("zzzz", "zzzz", mode="skip")["distance"] == 0
+
+
+def test_config1(golden):
+    a, b = W.cfg1()
+    got = L.compute(a, b)
+    for f in FIELDS:
+        assert got[f] == golden["configs"]["cfg1"]["report"][f], f
+
+
+def test_config3(golden):
+    a, b = W.cfg3()
+    got = L.compute(a, b)
+    for f in FIELDS:
+        assert got[f] == golden["configs"]["cfg3"]["report"][f], f
+
+
+def test_config4_preprocessed(golden):
+    a, b = W.cfg4()
+    got = L.compute(a, b, encoding="dna4", preprocess=True)
+    for f in FIELDS:
+        assert got[f] == golden["configs"]["cfg4"]["report"][f], f
+
+
+def test_config5_subset_batched(golden):
+    pairs = W.cfg5(8)
+    reps = L.compute_batch(pairs)
+    for rep, want in zip(reps, golden["configs"]["cfg5"][:8]):
+        for f in ("distance", "visited_cells", "pbs_equality", "pbs_kernel", "pbs_total",
+                  "refresh_count", "max_key_variance"):
+            assert rep[f] == want["report"][f], f
+
+
+def test_empty_operands():
+    assert L.compute("", "")["distance"] == 0
+    assert L.compute("abc", "")["distance"] == 3
+    assert L.compute("", "abcd")["distance"] == 4
+    with pytest.raises(L.BandTooNarrow):
+        L.compute("ab", "", mode="skip")
