@@ -1,0 +1,334 @@
+"""Benchmark: batched TFHE PBS on B200 (BASELINE.json configs[1], "cfg2").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+A step = one KS -> MS -> blind rotation -> sample extract pass over the
+4096-ciphertext cfg2 batch (identity LUT, messages from mt19937(1), keys
+from seed 0, n=880 N=2048). `value` is device-timed PBS/s with inputs
+resident in HBM (CUDA events on the library's stream, L2 flushed between
+steps); `e2e` is the same metric through the C ABI with pinned host
+buffers (lv_pbs_batch_host: H2D, KS, BR, SE, D2H per step). `roofline`
+reports the blind-rotation kernel against the FP64 FMA peak measured on
+this GPU. `cpu_baseline` is the CPU oracle (our C restatement of the PBS,
+"port") on the host cores. Extra keys report encrypted DP cells/s on the
+edit-distance configs.
+
+Multi-GPU (torchrun): every rank runs its own cfg2 batch (independent
+bootstraps; no data-path collective) -> "scaling": "weak"; rank 0 prints
+the max-over-ranks timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BATCH = 4096
+FLOP_PER_PBS = 209.0e6  # 3520 transforms x 5(N/2)log2(N/2) + MAC, FP64
+BSK_BYTES = 880 * 2 * 2 * 1024 * 16  # Fourier BSK streamed once per PBS by each item
+L2_FLUSH = 256 << 20
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def maybe_init_dist(ws, local):
+    if ws <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    return dist
+
+
+def reduce_max(dist, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier_sync(dist):
+    import torch
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._th = threading.Thread(target=run, daemon=True)
+        self._th.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=6)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for name, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def cpu_oracle_pbs_rate(sample: int, threads: int = 0):
+    """The oracle's PBS on host cores (kind 'port'): `sample` cfg2 items."""
+    from oracle import oracle as O
+    from paper_2508_14568_b200 import workloads as W
+    o = O.Oracle(0, threads=threads)
+    vals = W.cfg2()[:sample]
+    rows = np.stack([o.encrypt(v, i) for i, v in enumerate(vals)])
+    luts = np.tile(np.arange(16, dtype=np.int32), (sample, 1))
+    t0 = time.perf_counter()
+    out = o.pbs_batch(rows, luts, 0, threads)
+    dt = time.perf_counter() - t0
+    ok = all(o.decrypt(out[i]) == vals[i] for i in range(sample))
+    cores = threads if threads > 0 else (os.cpu_count() or 1)
+    return sample / dt, cores, dt, ok
+
+
+def reference_sim_rate():
+    """The reference's own SimBackend (oracle/_ref) on cfg2: a table lookup, no
+    cryptography — reported beside, never as, the PBS baseline."""
+    import ctypes
+    path = os.path.join(ROOT, "oracle", "_ref", "libleuven_ref.so")
+    if not os.path.exists(path):
+        return None
+    from paper_2508_14568_b200 import workloads as W
+    L = ctypes.CDLL(path)
+    L.ref_sim_pbs.restype = ctypes.c_double
+    L.ref_sim_pbs.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.c_uint64, ctypes.c_int,
+                              ctypes.POINTER(ctypes.c_int32)]
+    vals = W.cfg2()
+    arr = (ctypes.c_int32 * len(vals))(*vals)
+    res = (ctypes.c_int32 * len(vals))()
+    best = min(L.ref_sim_pbs(arr, len(vals), 1, res) for _ in range(5))
+    return {"value": len(vals) / best, "unit": "sim-PBS/s", "cores": 1, "kind": "reference",
+            "sample": "cfg2 4096 SimBackend::pbs calls (proj/src/backend.cpp:61-70): "
+                      "negacyclic_eval + ledger, no cryptography"}
+
+
+def traffic_from_profile():
+    p = os.path.join(ROOT, "profiles", "latest_br_ncu.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    sample = max(16, 4 * threads)
+    # each step: a bounded sample of the cfg2 batch on all host threads
+    for _ in range(max(1, min(args.warmup, 1))):
+        cpu_oracle_pbs_rate(min(sample, 16), threads)
+    rates = []
+    for _ in range(args.steps):
+        r, cores, dt, ok = cpu_oracle_pbs_rate(sample, threads)
+        rates.append(r)
+    v = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": "PBS/s (cfg2 batched programmable bootstrap)", "value": v,
+        "unit": "PBS/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sample / v * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
+        "config": {"workload": "cfg2: 4096 independent PBS, identity LUT, n=880 N=2048 k=1",
+                   "sample_per_step": sample},
+        "cpu_baseline": {"value": v, "unit": "PBS/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample} of the 4096 cfg2 PBS per step on {threads} threads "
+                                   "(oracle/tfhe_oracle.c, the CPU restatement; the reference's "
+                                   "SimBackend performs no cryptography, see reference_sim)"},
+        "e2e": {"value": v, "unit": "PBS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_sim": reference_sim_rate(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def dp_cells(ctx):
+    """Encrypted DP cells/s through compute() (encrypt -> GPU traversal -> decrypt)."""
+    import paper_2508_14568_b200 as L
+    from paper_2508_14568_b200 import workloads as W
+    out = {}
+    for name, fn, kw in (("cfg1", W.cfg1, {}), ("cfg3", W.cfg3, {}),
+                         ("cfg4", W.cfg4, {"encoding": "dna4", "preprocess": True})):
+        a, b = fn()
+        L.compute(a, b, ctx=ctx, **kw)  # warm (plan cache, scratch)
+        t0 = time.perf_counter()
+        r = L.compute(a, b, ctx=ctx, **kw)
+        dt = time.perf_counter() - t0
+        out[name] = {"cells": r["visited_cells"], "pbs": r["pbs_total"], "seconds": dt,
+                     "cells_per_s": r["visited_cells"] / dt, "pbs_per_s": r["pbs_total"] / dt,
+                     "distance": r["distance"], "waves": r["waves"]}
+    pairs = W.cfg5(16)
+    L.compute_batch(pairs[:2], ctx=ctx)
+    t0 = time.perf_counter()
+    reps = L.compute_batch(pairs, ctx=ctx)
+    dt = time.perf_counter() - t0
+    cells = sum(r["visited_cells"] for r in reps)
+    pbs = sum(r["pbs_total"] for r in reps)
+    out["cfg5_subset16"] = {"pairs": 16, "cells": cells, "pbs": pbs, "seconds": dt,
+                            "cells_per_s": cells / dt, "pbs_per_s": pbs / dt,
+                            "distances_sum": sum(r["distance"] for r in reps)}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extras", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+
+    import torch
+    import paper_2508_14568_b200 as L
+    from paper_2508_14568_b200 import workloads as W
+
+    dist = maybe_init_dist(ws, local)
+    torch.cuda.set_device(local)
+    ctx = L.Context(seed=0)
+    vals = W.cfg2(BATCH)
+    h = ctx.encrypt(vals)
+    lid = ctx.lut(L.identity_lut())
+    ids = np.full(BATCH, lid, np.uint32)
+    # correctness gate on the bench workload itself
+    out = ctx.pbs(h, lid)
+    assert list(ctx.decrypt(out)) == vals, "cfg2 decrypts wrong"
+    ctx.release(out)
+
+    ctx.bench_pbs(h, ids, max(3, args.warmup), L2_FLUSH)
+    barrier_sync(dist)
+    clk = ClockSampler(local)
+    clk.start()
+    br, ks, st = ctx.bench_pbs(h, ids, args.steps, L2_FLUSH)
+    barrier_sync(dist)
+    clocks = clk.stop()
+    ms_step = reduce_max(dist, float(np.mean(st)))
+    br_ms = reduce_max(dist, float(np.mean(br)))
+    ks_ms = reduce_max(dist, float(np.mean(ks)))
+    value = ws * BATCH / (ms_step / 1e3)
+
+    # e2e through the C ABI with pinned host buffers
+    rows = ctx.export(h)
+    pin_in = torch.from_numpy(rows).pin_memory()
+    pin_out = torch.empty_like(pin_in).pin_memory()
+    np_in, np_out = pin_in.numpy(), pin_out.numpy()
+    for _ in range(2):
+        ctx.pbs_host(np_in, ids, np_out)
+    barrier_sync(dist)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ctx.pbs_host(np_in, ids, np_out)
+    barrier_sync(dist)
+    e2e_s = reduce_max(dist, (time.perf_counter() - t0) / args.steps)
+    e2e_ok = all(int(x) == v for x, v in zip(ctx.decrypt(ctx.import_(np_out[:64])), vals[:64]))
+
+    peak = L.fp64_peak_tflops()
+    achieved = FLOP_PER_PBS * BATCH / (br_ms / 1e3) / 1e12
+    line = {
+        "metric": "PBS/s (cfg2 batched programmable bootstrap)", "value": value, "unit": "PBS/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64",
+        "data": "synthetic",
+        "config": {"workload": "cfg2: 4096 independent PBS, identity LUT, n=880 N=2048 k=1 "
+                               "(BSK 2^23x1, KSK 2^3x5)", "batch_per_gpu": BATCH,
+                   "keys_seed": 0, "messages": "mt19937(1) % 16",
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "parallelism": f"replica x{ws}"},
+        "kernel_ms": {"blind_rotate": br_ms, "keyswitch": ks_ms},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if peak else None, "traffic": traffic_from_profile(),
+                     "kernel": "blind_rotate_kernel",
+                     "note": "209 MFLOP/PBS algorithmic (5(N/2)log2(N/2) per transform + MAC); "
+                             "peak = DFMA throughput measured on this GPU by lv_bench_fp64_peak "
+                             "(MEASURED_PEAKS.json has no FP64 entry)",
+                     "hbm_view": {"bsk_bytes_per_pbs": BSK_BYTES,
+                                  "achieved_gbs": BSK_BYTES * BATCH / (br_ms / 1e3) / 1e9}},
+        "e2e": {"value": ws * BATCH / e2e_s, "unit": "PBS/s",
+                "h2d_bytes_per_step": int(rows.nbytes), "d2h_bytes_per_step": int(rows.nbytes),
+                "correct": bool(e2e_ok)},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clocks,
+    }
+    if rank == 0 and not args.no_extras:
+        try:
+            line["dp_cells"] = dp_cells(ctx)
+        except Exception as e:  # reported, never silently dropped
+            line["dp_cells"] = {"error": repr(e)}
+        try:
+            r, cores, dt, ok = cpu_oracle_pbs_rate(max(32, 4 * (os.cpu_count() or 1)))
+            line["cpu_baseline"] = {"value": r, "unit": "PBS/s", "cores": cores, "kind": "port",
+                                    "sample": f"{max(32, 4 * (os.cpu_count() or 1))} cfg2 PBS "
+                                              f"on {cores} threads in {dt:.1f}s, correct={ok}"}
+        except Exception as e:
+            line["cpu_baseline"] = {"error": repr(e)}
+        sim = reference_sim_rate()
+        if sim:
+            line["reference_sim"] = sim
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

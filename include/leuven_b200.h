@@ -184,7 +184,10 @@ int lv_debug_fft(lv_ctx* ctx, const int64_t* poly, double* spec, uint64_t* round
  * kernel, the key-switch kernel and the whole step (CUDA events on the
  * launching stream). */
 int lv_bench_pbs(lv_ctx* ctx, const lv_ct* in, const uint32_t* lut_ids, size_t count,
-                 int iters, float* br_ms, float* ks_ms, float* step_ms);
+                 int iters, uint64_t flush_bytes, float* br_ms, float* ks_ms, float* step_ms);
+/* Measured FP64 FMA throughput of this GPU (TFLOP/s, FMA = 2 flops): the
+ * denominator of the blind-rotation roofline. */
+int lv_bench_fp64_peak(float* tflops);
 
 #ifdef __cplusplus
 }

@@ -117,7 +117,7 @@ EXPORTS = [
     "lv_import", "lv_phase", "lv_pbs_batch_host", "lv_band_resolve", "lv_edit_distance_ee",
     "lv_edit_distance_batch", "lv_eq_table_build", "lv_eq_table_lookup", "lv_eq_table_destroy",
     "lv_edit_distance_pre", "lv_plan_trace", "lv_debug_keys", "lv_debug_keyswitch",
-    "lv_debug_blind_rotate", "lv_debug_fft", "lv_bench_pbs",
+    "lv_debug_blind_rotate", "lv_debug_fft", "lv_bench_pbs", "lv_bench_fp64_peak",
 ]
 
 _lib = None
@@ -182,9 +182,10 @@ def lib():
             "lv_debug_keyswitch": (ctypes.c_int, [vp, P(u64), sz, P(u64)]),
             "lv_debug_blind_rotate": (ctypes.c_int, [vp, P(u32), P(u32), sz, P(u64)]),
             "lv_debug_fft": (ctypes.c_int, [vp, P(i64), P(ctypes.c_double), P(u64)]),
-            "lv_bench_pbs": (ctypes.c_int, [vp, P(u32), P(u32), sz, ctypes.c_int,
+            "lv_bench_pbs": (ctypes.c_int, [vp, P(u32), P(u32), sz, ctypes.c_int, u64,
                                             P(ctypes.c_float), P(ctypes.c_float),
                                             P(ctypes.c_float)]),
+            "lv_bench_fp64_peak": (ctypes.c_int, [P(ctypes.c_float)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -340,7 +341,15 @@ class Context:
     def pbs(self, cts, lut):
         """Backend::pbs over a batch; ``lut`` is a Lut16 (entries) or an id array."""
         c = _u32(cts)
-        ids = np.full(c.size, self.lut(lut), np.uint32) if np.asarray(lut).size == 16 else _u32(lut)
+        la = np.asarray(lut)
+        if la.size == 16:
+            ids = np.full(c.size, self.lut(la), np.uint32)
+        elif la.ndim == 0:
+            ids = np.full(c.size, int(la), np.uint32)
+        else:
+            ids = _u32(la)
+        if ids.size != c.size:
+            raise InvalidParams("one lut id per ciphertext")
         out = np.zeros(c.size, np.uint32)
         _check(lib().lv_pbs_batch(self._h, _ptr(c, ctypes.c_uint32), _ptr(ids, ctypes.c_uint32),
                                   c.size, _ptr(out, ctypes.c_uint32)))
@@ -433,15 +442,21 @@ class Context:
                                   _ptr(rt, ctypes.c_uint64)))
         return spec, rt
 
-    def bench_pbs(self, cts, lut_ids, iters: int):
+    def bench_pbs(self, cts, lut_ids, iters: int, flush_bytes: int = 0):
         c, ids = _u32(cts), _u32(lut_ids)
         br = np.zeros(iters, np.float32)
         ks = np.zeros(iters, np.float32)
         st = np.zeros(iters, np.float32)
         _check(lib().lv_bench_pbs(self._h, _ptr(c, ctypes.c_uint32), _ptr(ids, ctypes.c_uint32), c.size,
-                                  iters, _ptr(br, ctypes.c_float), _ptr(ks, ctypes.c_float),
+                                  iters, flush_bytes, _ptr(br, ctypes.c_float), _ptr(ks, ctypes.c_float),
                                   _ptr(st, ctypes.c_float)))
         return br, ks, st
+
+
+def fp64_peak_tflops() -> float:
+    out = ctypes.c_float()
+    _check(lib().lv_bench_fp64_peak(ctypes.byref(out)))
+    return out.value
 
 
 from .leuven import (  # noqa: E402  (reference-shaped pipeline API)

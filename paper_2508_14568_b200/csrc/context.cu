@@ -781,8 +781,37 @@ int lv_debug_fft(lv_ctx* c, const int64_t* poly, double* spec, uint64_t* roundtr
   });
 }
 
+int lv_bench_fp64_peak(float* tflops) {
+  return guard([&] {
+    double* d = nullptr;
+    LV_CUDA(cudaMalloc(&d, 8));
+    int sms = 0, dev = 0;
+    LV_CUDA(cudaGetDevice(&dev));
+    LV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int blocks = sms * 8, threads = 256, iters = 8192;
+    cudaEvent_t e0, e1;
+    LV_CUDA(cudaEventCreate(&e0));
+    LV_CUDA(cudaEventCreate(&e1));
+    float best = 0;
+    for (int rep = 0; rep < 4; ++rep) {
+      LV_CUDA(cudaEventRecord(e0));
+      fp64_peak_kernel<<<blocks, threads>>>(d, iters, 1.0 + rep);
+      LV_CUDA(cudaEventRecord(e1));
+      LV_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      LV_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      const double flops = 2.0 * 8 * (double)iters * blocks * threads;
+      best = std::max(best, (float)(flops / (ms * 1e-3) / 1e12));
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d);
+    *tflops = best;
+  });
+}
+
 int lv_bench_pbs(lv_ctx* c, const lv_ct* in, const uint32_t* luts, size_t count, int iters,
-                 float* br_ms, float* ks_ms, float* step_ms) {
+                 uint64_t flush_bytes, float* br_ms, float* ks_ms, float* step_ms) {
   return guard([&] {
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     check_handles(c, in, count);
@@ -803,7 +832,10 @@ int lv_bench_pbs(lv_ctx* c, const lv_ct* in, const uint32_t* luts, size_t count,
     LV_CUDA(cudaEventCreate(&e0));
     LV_CUDA(cudaEventCreate(&e1));
     LV_CUDA(cudaEventCreate(&e2));
+    uint4* flush = nullptr;
+    if (flush_bytes) LV_CUDA(cudaMalloc(&flush, flush_bytes));
     for (int it = 0; it < iters; ++it) {
+      if (flush) flush_kernel<<<1184, 256, 0, c->stream>>>(flush, flush_bytes / 16);
       LV_CUDA(cudaEventRecord(e0, c->stream));
       launch_pbs_dev(c, dd, dl, dout, (uint32_t)count, e1);
       LV_CUDA(cudaEventRecord(e2, c->stream));
@@ -819,6 +851,7 @@ int lv_bench_pbs(lv_ctx* c, const lv_ct* in, const uint32_t* luts, size_t count,
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
+    if (flush) cudaFree(flush);
     pool_free(c, dst.data(), count);
     c->pbs_count += (uint64_t)count * iters;
   });

@@ -445,4 +445,26 @@ fft_backward_debug_kernel(const double2* spec, const double2* __restrict__ tw,
     }
 }
 
+// FP64 pipe peak microbenchmark: 8 independent DFMA chains per thread.
+__global__ void fp64_peak_kernel(double* out, int iters, double seed) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 1e-9 + k;
+  const double m = 0.999999999, c = 1e-12;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = __fma_rn(a[k], m, c);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 42.0) out[0] = s;
+}
+
+// L2 flush between timed iterations: write a buffer larger than L2.
+__global__ void flush_kernel(uint4* buf, size_t n16) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+    buf[i] = make_uint4((uint32_t)i, 0, 0, 0);
+}
+
 }  // namespace lvb

@@ -115,6 +115,9 @@ __global__ void fft_forward_debug_kernel(const int64_t* poly, const double2* tw,
 __global__ void fft_backward_debug_kernel(const double2* spec, const double2* tw,
                                           const double2* twist, uint64_t* poly);
 
+__global__ void fp64_peak_kernel(double* out, int iters, double seed);
+__global__ void flush_kernel(uint4* buf, size_t n16);
+
 constexpr int kKsItems = 16;
 
 }  // namespace lvb
