@@ -316,16 +316,35 @@ static void build_tables(orc_ctx* c) {
     c->tw[2 * t] = (double)cosl(ang);
     c->tw[2 * t + 1] = (double)(-sinl(ang));
   }
+  /* twist zeta^j = exp(i pi j / N), j < M, is DEFINED as the product of a
+   * fine table (j mod 128) and a coarse table (j div 128), each rounded from
+   * long double: the GPU keeps only the 2 KB fine table hot in L1. */
   c->twist = (double*)malloc(sizeof(double) * 2 * M);
   c->untwist = (double*)malloc(sizeof(double) * 2 * M);
-  for (uint32_t j = 0; j < M; ++j) {
+  const uint32_t FINE = 128, COARSE = M / FINE;
+  double* fine = (double*)malloc(sizeof(double) * 2 * FINE);
+  double* coarse = (double*)malloc(sizeof(double) * 2 * COARSE);
+  for (uint32_t j = 0; j < FINE; ++j) {
     long double ang = PI * (long double)j / (long double)N;
-    double cr = (double)cosl(ang), ci = (double)sinl(ang);
+    fine[2 * j] = (double)cosl(ang);
+    fine[2 * j + 1] = (double)sinl(ang);
+  }
+  for (uint32_t k = 0; k < COARSE; ++k) {
+    long double ang = PI * (long double)(k * FINE) / (long double)N;
+    coarse[2 * k] = (double)cosl(ang);
+    coarse[2 * k + 1] = (double)sinl(ang);
+  }
+  for (uint32_t j = 0; j < M; ++j) {
+    double cr, ci;
+    cmul(fine[2 * (j % FINE)], fine[2 * (j % FINE) + 1], coarse[2 * (j / FINE)],
+         coarse[2 * (j / FINE) + 1], &cr, &ci);
     c->twist[2 * j] = cr;
     c->twist[2 * j + 1] = ci;
     c->untwist[2 * j] = cr / (double)M;
     c->untwist[2 * j + 1] = -ci / (double)M;
   }
+  free(fine);
+  free(coarse);
 }
 
 /* ------------------------------------------------------------------ */

@@ -298,15 +298,26 @@ static void pbs_batch(lv_ctx* c, const lv_ct* in, const uint32_t* luts, size_t c
 
 static void build_tables(lv_ctx* c) {
   const long double PI = 3.141592653589793238462643383279502884L;
-  std::vector<double2> tw(kM / 2), twist(kM);
+  // W[k] = exp(-2 pi i k / kM), k < kM/2, then the per-stage copies
+  // T_s[y] = W[y << s] concatenated (fft.cuh tws()).
+  std::vector<double2> W(kM / 2), tw(kM), twist(128);
   for (uint32_t t = 0; t < kM / 2; ++t) {
     const long double ang = 2.0L * PI * (long double)t / (long double)kM;
-    tw[t] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
+    W[t] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
   }
-  for (uint32_t j = 0; j < kM; ++j) {
+  for (uint32_t s = 0; s < kLogM; ++s)
+    for (uint32_t y = 0; y < (kM >> (s + 1)); ++y) tw[(kM - (kM >> s)) + y] = W[y << s];
+  // twist zeta^j = fine[j & 127] * coarse[j >> 7] (oracle build_tables)
+  for (uint32_t j = 0; j < 128; ++j) {
     const long double ang = PI * (long double)j / (long double)kN;
     twist[j] = make_double2((double)cosl(ang), (double)sinl(ang));
   }
+  double2 coarse[8];
+  for (uint32_t k = 0; k < 8; ++k) {
+    const long double ang = PI * (long double)(k * 128) / (long double)kN;
+    coarse[k] = make_double2((double)cosl(ang), (double)sinl(ang));
+  }
+  set_twist_coarse(coarse);
   LV_CUDA(cudaMalloc(&c->d_tw, tw.size() * sizeof(double2)));
   LV_CUDA(cudaMalloc(&c->d_twist, twist.size() * sizeof(double2)));
   LV_CUDA(cudaMemcpy(c->d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));

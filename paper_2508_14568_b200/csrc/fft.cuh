@@ -77,8 +77,21 @@ __device__ __forceinline__ void dit1(double2& p, double2& q) {  // w = W[0]
   q = b;
 }
 
-__device__ __forceinline__ double2 ldtw(const double2* __restrict__ tw, uint32_t i) {
-  return __ldg(tw + i);
+// Per-stage twiddle tables T_s[y] = W[y << s] (W[k] = exp(-2 pi i k / kM)),
+// concatenated: T_s starts at kM - (kM >> s). Same values as W, laid out so
+// every warp-wide twiddle load is contiguous.
+__device__ __forceinline__ double2 tws(const double2* __restrict__ tw, int s, uint32_t y) {
+  return __ldg(tw + (kM - (kM >> s)) + y);
+}
+
+// Coarse twist factors zeta^(128 k), k < 8 (constant bank).
+__constant__ double2 c_twist_coarse[8];  // defined here: fft.cuh has one includer (kernels.cu)
+
+// zeta^x = fine[x & 127] * coarse[x >> 7] (oracle build_tables defines the
+// twist this way); coarse[0] = 1 is an exact identity and is skipped.
+__device__ __forceinline__ double2 twist_at(const double2* __restrict__ fine, uint32_t x) {
+  const double2 f = __ldg(fine + (x & 127));
+  return (x >> 7) == 0 ? f : cmul(f, c_twist_coarse[x >> 7]);
 }
 
 __device__ __forceinline__ double2 shfl_xor_d2(double2 v, int m) {
@@ -95,12 +108,12 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
   {
     double2 w0[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) w0[r] = ldtw(tw, t + 128 * r);
+    for (int r = 0; r < 4; ++r) w0[r] = tws(tw, 0, t + 128 * r);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 4; ++r) dif(X[p][r], X[p][r + 4], w0[r]);
-    const double2 w10 = ldtw(tw, t << 1), w11 = ldtw(tw, (t + 128) << 1);
+    const double2 w10 = tws(tw, 1, t), w11 = tws(tw, 1, t + 128);
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       dif(X[p][0], X[p][2], w10);
@@ -108,7 +121,7 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
       dif(X[p][4], X[p][6], w10);
       dif(X[p][5], X[p][7], w11);
     }
-    const double2 w2 = ldtw(tw, t << 2);
+    const double2 w2 = tws(tw, 2, t);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -128,12 +141,12 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
       for (int r = 0; r < 8; ++r) X[p][r] = buf[p * kM + swz(128 * b + u + 16 * r)];
     double2 w3[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) w3[r] = ldtw(tw, (u + 16 * r) << 3);
+    for (int r = 0; r < 4; ++r) w3[r] = tws(tw, 3, u + 16 * r);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 4; ++r) dif(X[p][r], X[p][r + 4], w3[r]);
-    const double2 w40 = ldtw(tw, u << 4), w41 = ldtw(tw, (u + 16) << 4);
+    const double2 w40 = tws(tw, 4, u), w41 = tws(tw, 4, u + 16);
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       dif(X[p][0], X[p][2], w40);
@@ -141,7 +154,7 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
       dif(X[p][4], X[p][6], w40);
       dif(X[p][5], X[p][7], w41);
     }
-    const double2 w5 = ldtw(tw, u << 5);
+    const double2 w5 = tws(tw, 5, u);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -161,12 +174,12 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
       for (int r = 0; r < 8; ++r) X[p][r] = buf[p * kM + swz(16 * c + v + 2 * r)];
     double2 w6[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) w6[r] = ldtw(tw, (v + 2 * r) << 6);
+    for (int r = 0; r < 4; ++r) w6[r] = tws(tw, 6, v + 2 * r);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 4; ++r) dif(X[p][r], X[p][r + 4], w6[r]);
-    const double2 w70 = ldtw(tw, v << 7), w71 = ldtw(tw, (v + 2) << 7);
+    const double2 w70 = tws(tw, 7, v), w71 = tws(tw, 7, v + 2);
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       dif(X[p][0], X[p][2], w70);
@@ -174,7 +187,7 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
       dif(X[p][4], X[p][6], w70);
       dif(X[p][5], X[p][7], w71);
     }
-    const double2 w8 = ldtw(tw, v << 8);
+    const double2 w8 = tws(tw, 8, v);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -214,7 +227,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&X)[P][8], double2* buf,
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; r += 2) dit1(X[p][r], X[p][r + 1]);
-    const double2 w81 = ldtw(tw, 1u << 8);
+    const double2 w81 = tws(tw, 8, 1);
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       dit1(X[p][0], X[p][2]);
@@ -222,7 +235,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&X)[P][8], double2* buf,
       dit1(X[p][4], X[p][6]);
       dit(X[p][5], X[p][7], w81);
     }
-    const double2 w71 = ldtw(tw, 1u << 7), w72 = ldtw(tw, 2u << 7), w73 = ldtw(tw, 3u << 7);
+    const double2 w71 = tws(tw, 7, 1), w72 = tws(tw, 7, 2), w73 = tws(tw, 7, 3);
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       dit1(X[p][0], X[p][4]);
@@ -242,12 +255,12 @@ __device__ __forceinline__ void fft_inverse(double2 (&X)[P][8], double2* buf,
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; ++r) X[p][r] = buf[p * kM + swz(64 * b + u + 8 * r)];
-    const double2 w6 = ldtw(tw, u << 6);
+    const double2 w6 = tws(tw, 6, u);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w6);
-    const double2 w50 = ldtw(tw, u << 5), w51 = ldtw(tw, (u + 8) << 5);
+    const double2 w50 = tws(tw, 5, u), w51 = tws(tw, 5, u + 8);
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       dit(X[p][0], X[p][2], w50);
@@ -257,7 +270,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&X)[P][8], double2* buf,
     }
     double2 w4[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) w4[r] = ldtw(tw, (u + 8 * r) << 4);
+    for (int r = 0; r < 4; ++r) w4[r] = tws(tw, 4, u + 8 * r);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -275,12 +288,12 @@ __device__ __forceinline__ void fft_inverse(double2 (&X)[P][8], double2* buf,
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; ++r) X[p][r] = buf[p * kM + swz(512 * h + u + 64 * r)];
-    const double2 w3 = ldtw(tw, u << 3);
+    const double2 w3 = tws(tw, 3, u);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w3);
-    const double2 w20 = ldtw(tw, u << 2), w21 = ldtw(tw, (u + 64) << 2);
+    const double2 w20 = tws(tw, 2, u), w21 = tws(tw, 2, u + 64);
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       dit(X[p][0], X[p][2], w20);
@@ -290,7 +303,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&X)[P][8], double2* buf,
     }
     double2 w1[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) w1[r] = ldtw(tw, (u + 64 * r) << 1);
+    for (int r = 0; r < 4; ++r) w1[r] = tws(tw, 1, u + 64 * r);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -298,7 +311,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&X)[P][8], double2* buf,
     // stage 0 (half 512): lane pairs (t, t^16) hold x and x + 512.
     double2 w0[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) w0[q] = ldtw(tw, u + 64 * (4 * h + q));
+    for (int q = 0; q < 4; ++q) w0[q] = tws(tw, 0, u + 64 * (4 * h + q));
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       double2 Y[4];

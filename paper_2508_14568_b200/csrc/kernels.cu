@@ -17,6 +17,20 @@
 
 namespace lvb {
 
+
+void set_twist_coarse(const double2* host8) {
+  cudaMemcpyToSymbol(c_twist_coarse, host8, 8 * sizeof(double2));
+}
+
+// Streaming read of the Fourier BSK: no L1 allocation, so the twiddle tables
+// stay resident in L1 (the BSK itself is L2-resident, 57.7 MB < 126 MB).
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
 // ------------------------------------------------------------------ BR
 // One CTA (128 threads) blind-rotates one item: ACC = X^{-b~} (0, TP), then
 // for every small-key coefficient i: ACC += BSK_i [x] (X^{a~_i} ACC - ACC),
@@ -70,10 +84,11 @@ blind_rotate_kernel(BrArgs a) {
         for (int hpart = 0; hpart < 2; ++hpart) {
           const uint32_t j = x + hpart * kM;
           const uint32_t s = (j + 2 * kN - rot) & (2 * kN - 1);
-          const uint64_t rv = s < kN ? P[s] : (uint64_t)0 - P[s - kN];
+          const uint64_t pv = P[s & (kN - 1)];  // one load; the wrap only flips the sign
+          const uint64_t rv = s < kN ? pv : (uint64_t)0 - pv;
           d[hpart] = decomp1(rv - P[j], kPbsBaseLog);
         }
-        X[p][r] = cmul(make_double2((double)d[0], (double)d[1]), __ldg(twist + x));
+        X[p][r] = cmul(make_double2((double)d[0], (double)d[1]), twist_at(twist, x));
       }
     }
 
@@ -84,10 +99,10 @@ blind_rotate_kernel(BrArgs a) {
       const double2* bsk = a.bskf + (size_t)i * (32 * 128) + t;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const double2 b00 = __ldg(bsk + (q * 4 + 0) * 128);
-        const double2 b01 = __ldg(bsk + (q * 4 + 1) * 128);
-        const double2 b10 = __ldg(bsk + (q * 4 + 2) * 128);
-        const double2 b11 = __ldg(bsk + (q * 4 + 3) * 128);
+        const double2 b00 = ld_stream(bsk + (q * 4 + 0) * 128);
+        const double2 b01 = ld_stream(bsk + (q * 4 + 1) * 128);
+        const double2 b10 = ld_stream(bsk + (q * 4 + 2) * 128);
+        const double2 b11 = ld_stream(bsk + (q * 4 + 3) * 128);
         const double2 d0 = X[0][q], d1 = X[1][q];
         double2 o0, o1;
         o0.x = __fma_rn(d0.x, b00.x, 0.0);
@@ -121,7 +136,7 @@ blind_rotate_kernel(BrArgs a) {
 #pragma unroll
         for (int hi = 0; hi < 2; ++hi) {
           const uint32_t x = u + 64 * (4 * h + q) + 512 * hi;
-          const double2 tv = __ldg(twist + x);
+          const double2 tv = twist_at(twist, x);
           const double2 ut = make_double2(__dmul_rn(tv.x, 0x1p-10), __dmul_rn(-tv.y, 0x1p-10));
 #pragma unroll
           for (int p = 0; p < 2; ++p) {
@@ -392,7 +407,7 @@ bsk_fourier_kernel(const uint64_t* bsk, const double2* __restrict__ tw,
       const uint32_t x = t + 128 * q;
       const double re = (double)(int64_t)poly[x];
       const double im = (double)(int64_t)poly[x + kM];
-      X[o][q] = cmul(make_double2(re, im), __ldg(twist + x));
+      X[o][q] = cmul(make_double2(re, im), twist_at(twist, x));
     }
   }
   fft_forward<2>(X, buf, tw, t);
@@ -414,7 +429,7 @@ fft_forward_debug_kernel(const int64_t* poly, const double2* __restrict__ tw,
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const uint32_t x = t + 128 * q;
-    X[0][q] = cmul(make_double2((double)poly[x], (double)poly[x + kM]), __ldg(twist + x));
+    X[0][q] = cmul(make_double2((double)poly[x], (double)poly[x + kM]), twist_at(twist, x));
   }
   fft_forward<1>(X, buf, tw, t);
 #pragma unroll
@@ -437,7 +452,7 @@ fft_backward_debug_kernel(const double2* spec, const double2* __restrict__ tw,
 #pragma unroll
     for (int hi = 0; hi < 2; ++hi) {
       const uint32_t x = u + 64 * (4 * h + q) + 512 * hi;
-      const double2 tv = __ldg(twist + x);
+      const double2 tv = twist_at(twist, x);
       const double2 ut = make_double2(__dmul_rn(tv.x, 0x1p-10), __dmul_rn(-tv.y, 0x1p-10));
       const double2 z = cmul(X[0][4 * hi + q], ut);
       poly[x] = f64_to_torus(z.x);

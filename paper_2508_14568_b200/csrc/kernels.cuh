@@ -50,8 +50,8 @@ struct BrArgs {
   const uint32_t* lut_of_item; // [count] test polynomial index
   const uint64_t* test_polys;  // [luts][N]
   const double2* bskf;         // Fourier BSK, MAC layout
-  const double2* twiddles;     // W[t], t < kM/2
-  const double2* twist;        // zeta^j, j < kM
+  const double2* twiddles;     // per-stage tables T_s (fft.cuh)
+  const double2* twist;        // fine twist table zeta^j, j < 128
   uint32_t n;
   uint64_t* pool;              // pool base
   uint32_t pool_stride;
@@ -117,6 +117,8 @@ __global__ void fft_backward_debug_kernel(const double2* spec, const double2* tw
 
 __global__ void fp64_peak_kernel(double* out, int iters, double seed);
 __global__ void flush_kernel(uint4* buf, size_t n16);
+
+void set_twist_coarse(const double2* host8);
 
 constexpr int kKsItems = 16;
 
