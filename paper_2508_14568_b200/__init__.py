@@ -19,7 +19,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libleuven_b200.so")
+# LVB_LIB overrides the library (experiment variants built by build.py --out)
+LIB_PATH = os.environ.get("LVB_LIB", os.path.join(HERE, "_build", "libleuven_b200.so"))
 
 # ----------------------------------------------------------------- errors
 # One class per reference exception (proj/include/leuven/errors.hpp:8-39).

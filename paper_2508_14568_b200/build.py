@@ -37,25 +37,34 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(OUT, exist_ok=True)
+def build(verbose: bool = False, defines=(), out_dir: str = OUT) -> str:
+    """defines: extra -D flags for experiment variants (built into out_dir)."""
+    os.makedirs(out_dir, exist_ok=True)
+    lib = os.path.join(out_dir, "libleuven_b200.so")
     objs = []
     hdrs = _headers()
     for src in SOURCES:
         path = os.path.join(CSRC, src)
-        obj = os.path.join(OUT, src + ".o")
+        obj = os.path.join(out_dir, src + ".o")
         objs.append(obj)
         if _stale(obj, [path] + hdrs):
             lang = ["-x", "cu"] if src.endswith(".cpp") else []
-            cmd = [NVCC] + ARCH + FLAGS + lang + ["-c", path, "-o", obj]
+            cmd = [NVCC] + ARCH + FLAGS + ["-D" + d for d in defines] + lang + ["-c", path, "-o", obj]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
             subprocess.run(cmd, check=True)
-    if _stale(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+    if _stale(lib, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart"]
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose=True))
+    # python build.py [DEFINE=VAL ...] [--out DIR]
+    args = sys.argv[1:]
+    out = OUT
+    if "--out" in args:
+        i = args.index("--out")
+        out = args[i + 1]
+        args = args[:i] + args[i + 2:]
+    print(build(verbose=True, defines=args, out_dir=out))

@@ -135,7 +135,7 @@ void launch_pbs_dev(lv_ctx* c, const LinDesc* d_desc, const uint32_t* d_lut, con
   if (!count) return;
   const uint32_t stride = ms_stride(c);
   uint16_t* d_ms = c->ms.get((size_t)count * stride);
-  KsArgs ka{d_desc, c->d_pool, kBigStride, c->d_ksk, c->p.n, count, d_ms, stride, nullptr};
+  KsArgs ka{d_desc, c->d_pool, kBigStride, c->d_ksk, c->d_ksk_bias, c->p.n, count, d_ms, stride, nullptr};
   const uint32_t row = c->p.n + 1;
   for (uint32_t off = 0; off < count; off += 65535u * kKsItems) {
     const uint32_t cnt = std::min<uint32_t>(count - off, 65535u * kKsItems);
@@ -335,6 +335,9 @@ static void keygen(lv_ctx* c) {
   keygen_ksk_kernel<<<kBig * kKsLevel, 256, 0, c->stream>>>(c->seed, n, c->p.lwe_noise_log2,
                                                             c->d_sk_small, c->d_sk_glwe, c->d_ksk);
   LV_CUDA(cudaGetLastError());
+  LV_CUDA(cudaMalloc(&c->d_ksk_bias, (size_t)(n + 1) * sizeof(uint64_t)));
+  ksk_bias_kernel<<<(n + 1 + 127) / 128, 128, 0, c->stream>>>(c->d_ksk, n, c->d_ksk_bias);
+  LV_CUDA(cudaGetLastError());
   uint64_t* d_bsk = nullptr;
   LV_CUDA(cudaMalloc(&d_bsk, (size_t)n * kRows * (kK + 1) * kN * sizeof(uint64_t)));
   keygen_bsk_kernel<<<n * kRows, 256, 0, c->stream>>>(c->seed, c->p.glwe_noise_log2, c->d_sk_small,
@@ -440,7 +443,7 @@ int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
 void lv_ctx_destroy(lv_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (void* p : {(void*)c->d_sk_small, (void*)c->d_sk_glwe, (void*)c->d_ksk, (void*)c->d_bskf,
+  for (void* p : {(void*)c->d_sk_small, (void*)c->d_sk_glwe, (void*)c->d_ksk, (void*)c->d_ksk_bias, (void*)c->d_bskf,
                   (void*)c->d_tw, (void*)c->d_twist, (void*)c->d_tp, (void*)c->d_pool})
     if (p) cudaFree(p);
   c->ms.release();
@@ -733,7 +736,7 @@ int lv_debug_keyswitch(lv_ctx* c, const uint64_t* in, size_t count, uint64_t* ou
     const uint32_t row = c->p.n + 1, stride = ms_stride(c);
     uint64_t* dsmall = c->u64b.get(count * row);
     uint16_t* dms = c->ms.get(count * stride);
-    KsArgs ka{dd, c->d_pool, kBigStride, c->d_ksk, c->p.n, (uint32_t)count, dms, stride, dsmall};
+    KsArgs ka{dd, c->d_pool, kBigStride, c->d_ksk, c->d_ksk_bias, c->p.n, (uint32_t)count, dms, stride, dsmall};
     dim3 grid((row + 127) / 128, (uint32_t)((count + kKsItems - 1) / kKsItems));
     keyswitch_kernel<<<grid, 128, 0, c->stream>>>(ka);
     LV_CUDA(cudaGetLastError());

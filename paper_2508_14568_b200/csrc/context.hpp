@@ -73,6 +73,7 @@ struct lv_ctx {
   uint8_t* d_sk_small = nullptr;
   uint8_t* d_sk_glwe = nullptr;
   uint64_t* d_ksk = nullptr;
+  uint64_t* d_ksk_bias = nullptr;
   double2* d_bskf = nullptr;
   double2* d_tw = nullptr;
   double2* d_twist = nullptr;

@@ -34,6 +34,42 @@ __device__ __forceinline__ uint32_t swz(uint32_t x) {
   return x ^ ((((x >> 3) & 7u) ^ (((x >> 9) & 1u) << 2)));
 }
 
+// Exchange through shared memory: one polynomial at a time through a
+// single kM-entry buffer (16 KB) instead of all P at once, so the blind
+// rotation fits 4 CTAs per SM. Set LVB_SPLIT_XCHG=0 for the P-buffer form.
+#ifndef LVB_SPLIT_XCHG
+#define LVB_SPLIT_XCHG 1
+#endif
+constexpr bool kSplitXchg = LVB_SPLIT_XCHG;
+constexpr int kXchgBufs = kSplitXchg ? 1 : 2;
+
+// Moves X from layout wr(r) to layout rd(r) (element indices x); the caller
+// guarantees the buffer is free on entry.
+template <int P, typename WR, typename RD>
+__device__ __forceinline__ void xchg(double2 (&X)[P][8], double2* buf, WR wr, RD rd) {
+  if constexpr (!kSplitXchg || P == 1) {
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) buf[p * kM + swz(wr(r))] = X[p][r];
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) X[p][r] = buf[p * kM + swz(rd(r))];
+  } else {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (p) __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 8; ++r) buf[swz(wr(r))] = X[p][r];
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 8; ++r) X[p][r] = buf[swz(rd(r))];
+    }
+  }
+}
+
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   const double t1 = __dmul_rn(a.y, b.y);
   const double t2 = __dmul_rn(a.y, b.x);
@@ -128,17 +164,10 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
       for (int r = 0; r < 8; r += 2) dif(X[p][r], X[p][r + 1], w2);
   }
   // A -> B
-#pragma unroll
-  for (int p = 0; p < P; ++p)
-#pragma unroll
-    for (int r = 0; r < 8; ++r) buf[p * kM + swz(t + 128 * r)] = X[p][r];
-  __syncthreads();
   {
     const uint32_t b = t >> 4, u = t & 15;
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int r = 0; r < 8; ++r) X[p][r] = buf[p * kM + swz(128 * b + u + 16 * r)];
+    xchg<P>(X, buf, [&](int r) { return t + 128 * r; },
+            [&](int r) { return 128 * b + u + 16 * r; });
     double2 w3[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) w3[r] = tws(tw, 3, u + 16 * r);
@@ -160,18 +189,12 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
 #pragma unroll
       for (int r = 0; r < 8; r += 2) dif(X[p][r], X[p][r + 1], w5);
     __syncthreads();
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int r = 0; r < 8; ++r) buf[p * kM + swz(128 * b + u + 16 * r)] = X[p][r];
-  }
-  __syncthreads();
-  {
     const uint32_t c = t >> 1, v = t & 1;
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int r = 0; r < 8; ++r) X[p][r] = buf[p * kM + swz(16 * c + v + 2 * r)];
+    xchg<P>(X, buf, [&](int r) { return 128 * b + u + 16 * r; },
+            [&](int r) { return 16 * c + v + 2 * r; });
+  }
+  {
+    const uint32_t v = t & 1;
     double2 w6[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) w6[r] = tws(tw, 6, v + 2 * r);
@@ -244,17 +267,9 @@ __device__ __forceinline__ void fft_inverse(double2 (&X)[P][8], double2* buf,
       dit(X[p][3], X[p][7], w73);
     }
   }
-#pragma unroll
-  for (int p = 0; p < P; ++p)
-#pragma unroll
-    for (int r = 0; r < 8; ++r) buf[p * kM + swz(8 * t + r)] = X[p][r];
-  __syncthreads();
   {
     const uint32_t b = t >> 3, u = t & 7;
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int r = 0; r < 8; ++r) X[p][r] = buf[p * kM + swz(64 * b + u + 8 * r)];
+    xchg<P>(X, buf, [&](int r) { return 8 * t + r; }, [&](int r) { return 64 * b + u + 8 * r; });
     const double2 w6 = tws(tw, 6, u);
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -276,18 +291,12 @@ __device__ __forceinline__ void fft_inverse(double2 (&X)[P][8], double2* buf,
 #pragma unroll
       for (int r = 0; r < 4; ++r) dit(X[p][r], X[p][r + 4], w4[r]);
     __syncthreads();
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int r = 0; r < 8; ++r) buf[p * kM + swz(64 * b + u + 8 * r)] = X[p][r];
+    const uint32_t h = (t >> 4) & 1, u2 = 16 * (t >> 5) + (t & 15);
+    xchg<P>(X, buf, [&](int r) { return 64 * b + u + 8 * r; },
+            [&](int r) { return 512 * h + u2 + 64 * r; });
   }
-  __syncthreads();
   {
     const uint32_t h = (t >> 4) & 1, u = 16 * (t >> 5) + (t & 15);
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int r = 0; r < 8; ++r) X[p][r] = buf[p * kM + swz(512 * h + u + 64 * r)];
     const double2 w3 = tws(tw, 3, u);
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -332,7 +341,9 @@ __device__ __forceinline__ void fft_inverse(double2 (&X)[P][8], double2* buf,
   }
 }
 
-// f64 -> Z_{2^64}, identical to oracle f64_to_torus.
+// f64 -> Z_{2^64}, identical to oracle f64_to_torus. (An integer-pipe
+// variant — exponent/mantissa shift for |y| >= 2^52 — measured slower on
+// B200, 87-90 ms vs 82.5 ms per 4096 PBS, and was dropped.)
 __device__ __forceinline__ uint64_t f64_to_torus(double y) {
   const double two64 = 18446744073709551616.0;
   const double r = rint(__dmul_rn(y, 0x1p-64));

@@ -36,14 +36,17 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
 // for every small-key coefficient i: ACC += BSK_i [x] (X^{a~_i} ACC - ACC),
 // then sample-extracts coefficient 0 into a big-key LWE.
 //
-// Shared memory: acc[2][N] u64 (32 KB) + FFT exchange buffer 2 x kM double2
-// (32 KB) + ms[n+1] u16.
-__global__ void __launch_bounds__(128, 3)
+// Shared memory: acc[2][N] u64 (32 KB) + FFT exchange buffer kXchgBufs x kM
+// double2 (16 KB split / 32 KB) + ms[n+1] u16.
+#ifndef LVB_BR_MIN_BLOCKS
+#define LVB_BR_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(128, LVB_BR_MIN_BLOCKS)
 blind_rotate_kernel(BrArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* acc = reinterpret_cast<uint64_t*>(smem);                   // [2][kN]
-  double2* buf = reinterpret_cast<double2*>(smem + 2 * kN * 8);        // [2][kM]
-  uint16_t* ms = reinterpret_cast<uint16_t*>(smem + 2 * kN * 8 + 2 * kM * 16);
+  double2* buf = reinterpret_cast<double2*>(smem + 2 * kN * 8);        // [kXchgBufs][kM]
+  uint16_t* ms = reinterpret_cast<uint16_t*>(smem + 2 * kN * 8 + kXchgBufs * kM * 16);
   const uint32_t t = threadIdx.x;
   const uint32_t item = blockIdx.x;
   const uint32_t n = a.n;
@@ -79,14 +82,14 @@ blind_rotate_kernel(BrArgs a) {
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const uint32_t x = t + 128 * r;
-        int64_t d[2];
+        int32_t d[2];  // |digit| <= 2^22: int32 -> f64 conversion is exact
 #pragma unroll
         for (int hpart = 0; hpart < 2; ++hpart) {
           const uint32_t j = x + hpart * kM;
           const uint32_t s = (j + 2 * kN - rot) & (2 * kN - 1);
           const uint64_t pv = P[s & (kN - 1)];  // one load; the wrap only flips the sign
           const uint64_t rv = s < kN ? pv : (uint64_t)0 - pv;
-          d[hpart] = decomp1(rv - P[j], kPbsBaseLog);
+          d[hpart] = (int32_t)decomp1(rv - P[j], kPbsBaseLog);
         }
         X[p][r] = cmul(make_double2((double)d[0], (double)d[1]), twist_at(twist, x));
       }
@@ -136,6 +139,7 @@ blind_rotate_kernel(BrArgs a) {
 #pragma unroll
         for (int hi = 0; hi < 2; ++hi) {
           const uint32_t x = u + 64 * (4 * h + q) + 512 * hi;
+          // untwist = conj(twist) / M (exact power-of-two scaling)
           const double2 tv = twist_at(twist, x);
           const double2 ut = make_double2(__dmul_rn(tv.x, 0x1p-10), __dmul_rn(-tv.y, 0x1p-10));
 #pragma unroll
@@ -178,7 +182,7 @@ blind_rotate_kernel(BrArgs a) {
 }
 
 size_t blind_rotate_smem_bytes(uint32_t n) {
-  return 2 * kN * 8 + 2 * kM * 16 + ((n + 1) * 2 + 15) / 16 * 16;
+  return 2 * kN * 8 + kXchgBufs * kM * 16 + ((n + 1) * 2 + 15) / 16 * 16;
 }
 
 // ------------------------------------------------------------------ KS
@@ -187,8 +191,15 @@ size_t blind_rotate_smem_bytes(uint32_t n) {
 // modulus switch to 2N. Tile: KS_ITEMS items x 128 output coefficients per
 // CTA; the items' digits for a chunk of 32 input coefficients are staged in
 // shared memory and every KSK element loaded is reused across the tile.
-constexpr int KS_ITEMS = 16;
+//
+// Digits d in [-4, 4) are stored biased, u = d + 4 in [0, 8) (one nibble,
+// 8 items per 32-bit word), so each multiply-accumulate is an unsigned
+// 32x64 -> 64 product (IMAD.WIDE.U32 + IMAD); the bias is paid back once:
+//   sum_j,l -d K[j][l][c] = ksk_bias[c] - sum_j,l u K[j][l][c],
+//   ksk_bias[c] = 4 sum_j,l K[j][l][c]   (exact in Z_2^64; keygen computes it).
+constexpr int KS_ITEMS = kKsItems;
 constexpr int KS_CHUNK = 32;
+static_assert(KS_ITEMS == 32, "nibble packing assumes 4 words of 8 items");
 
 __device__ __forceinline__ uint64_t lin_coef(const LinDesc& d, const uint64_t* pool,
                                              uint32_t stride, uint32_t j) {
@@ -201,7 +212,7 @@ __device__ __forceinline__ uint64_t lin_coef(const LinDesc& d, const uint64_t* p
 
 __global__ void __launch_bounds__(128)
 keyswitch_kernel(KsArgs a) {
-  __shared__ int8_t dig[KS_ITEMS][KS_CHUNK][kKsLevel];
+  __shared__ __align__(16) uint32_t dig[KS_CHUNK][kKsLevel][4];  // nibble-packed u = d + 4
   __shared__ LinDesc desc[KS_ITEMS];
   const uint32_t t = threadIdx.x;
   const uint32_t c = blockIdx.x * 128 + t;  // output coefficient
@@ -221,13 +232,22 @@ keyswitch_kernel(KsArgs a) {
 
   for (uint32_t j0 = 0; j0 < kBig; j0 += KS_CHUNK) {
     __syncthreads();
-    for (uint32_t e = t; e < KS_ITEMS * KS_CHUNK; e += 128) {
-      const uint32_t it = e / KS_CHUNK, jj = e % KS_CHUNK;
-      int64_t dd[kKsLevel];
-      const uint64_t v = (item0 + it < a.count) ? lin_coef(desc[it], a.pool, a.pool_stride, j0 + jj) : 0;
-      decomp<kKsLevel>(v, kKsBaseLog, dd);
+    {
+      // thread -> (jj, group of 8 items); one packed word per level
+      const uint32_t jj = t % KS_CHUNK, g = t / KS_CHUNK;
+      uint32_t w[kKsLevel] = {};
 #pragma unroll
-      for (int l = 0; l < (int)kKsLevel; ++l) dig[it][jj][l] = (int8_t)dd[l];
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t it = g * 8 + q;
+        const uint64_t v =
+            (item0 + it < a.count) ? lin_coef(desc[it], a.pool, a.pool_stride, j0 + jj) : 0;
+        int64_t dd[kKsLevel];
+        decomp<kKsLevel>(v, kKsBaseLog, dd);
+#pragma unroll
+        for (int l = 0; l < (int)kKsLevel; ++l) w[l] |= (uint32_t)(dd[l] + 4) << (4 * q);
+      }
+#pragma unroll
+      for (int l = 0; l < (int)kKsLevel; ++l) dig[jj][l][g] = w[l];
     }
     __syncthreads();
     if (c < row) {
@@ -235,19 +255,24 @@ keyswitch_kernel(KsArgs a) {
 #pragma unroll
         for (int l = 0; l < (int)kKsLevel; ++l) {
           const uint64_t kv = __ldg(a.ksk + ((size_t)(j0 + jj) * kKsLevel + l) * row + c);
+          const uint4 pk = *reinterpret_cast<const uint4*>(dig[jj][l]);
+          const uint32_t words[4] = {pk.x, pk.y, pk.z, pk.w};
 #pragma unroll
-          for (int it = 0; it < KS_ITEMS; ++it)
-            acc[it] -= (uint64_t)(int64_t)dig[it][jj][l] * kv;
+          for (int it = 0; it < KS_ITEMS; ++it) {
+            const uint32_t u = (words[it >> 3] >> (4 * (it & 7))) & 15u;
+            acc[it] += (uint64_t)u * kv;
+          }
         }
       }
     }
   }
   if (c >= row) return;
+  const uint64_t bias = a.ksk_bias[c];
 #pragma unroll
   for (int it = 0; it < KS_ITEMS; ++it) {
     const uint32_t item = item0 + it;
     if (item >= a.count) break;
-    uint64_t v = acc[it];
+    uint64_t v = bias - acc[it];
     if (c == n) v += lin_coef(desc[it], a.pool, a.pool_stride, kBig);
     if (a.small_out) a.small_out[(size_t)item * row + c] = v;
     a.ms[(size_t)item * a.ms_stride + c] = (uint16_t)modswitch(v);
@@ -351,6 +376,16 @@ __global__ void keygen_ksk_kernel(uint64_t seed, uint32_t n, uint32_t noise_log2
     if (sk_glwe[j]) b += 1ull << (64 - kKsBaseLog * (l + 1));
     row[n] = b;
   }
+}
+
+// bias[c] = 4 * sum over all KSK rows of column c (the unsigned-digit
+// key switch pays back its +4 digit offset with it).
+__global__ void ksk_bias_kernel(const uint64_t* ksk, uint32_t n, uint64_t* bias) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > n) return;
+  uint64_t s = 0;
+  for (uint32_t r = 0; r < kBig * kKsLevel; ++r) s += ksk[(size_t)r * (n + 1) + c];
+  bias[c] = 4 * s;
 }
 
 // One CTA (256 threads) per GGSW row (i, r): GLWE_S(0) + s_i * g on component r.

@@ -63,6 +63,7 @@ struct KsArgs {
   const uint64_t* pool;
   uint32_t pool_stride;
   const uint64_t* ksk;  // [kN][ks_level][n+1]
+  const uint64_t* ksk_bias;  // [n+1] 4 * sum_j,l ksk[j][l][c]
   uint32_t n;
   uint32_t count;
   uint16_t* ms;         // [count][ms_stride]
@@ -104,6 +105,7 @@ __global__ void linear_kernel(LinArgs a);
 __global__ void encrypt_kernel(EncArgs a);
 __global__ void phase_kernel(PhaseArgs a);
 __global__ void keygen_secret_kernel(uint64_t seed, uint32_t n, uint8_t* sk_small, uint8_t* sk_glwe);
+__global__ void ksk_bias_kernel(const uint64_t* ksk, uint32_t n, uint64_t* bias);
 __global__ void keygen_ksk_kernel(uint64_t seed, uint32_t n, uint32_t noise_log2,
                                   const uint8_t* sk_small, const uint8_t* sk_glwe, uint64_t* ksk);
 __global__ void keygen_bsk_kernel(uint64_t seed, uint32_t noise_log2, const uint8_t* sk_small,
@@ -120,6 +122,6 @@ __global__ void flush_kernel(uint4* buf, size_t n16);
 
 void set_twist_coarse(const double2* host8);
 
-constexpr int kKsItems = 16;
+constexpr int kKsItems = 32;
 
 }  // namespace lvb
