@@ -304,7 +304,7 @@ def main():
         "e2e": {"value": ws * BATCH / e2e_s, "unit": "PBS/s",
                 "h2d_bytes_per_step": int(rows.nbytes), "d2h_bytes_per_step": int(rows.nbytes),
                 "correct": bool(e2e_ok)},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": 3 * args.steps,  # per step: ks_digits, ks_mma (tcgen05), blind_rotate
         "clocks": clocks,
     }
     if rank == 0 and not args.no_extras:

@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["kernels.cu", "context.cu", "wavefront.cu", "ledger.cpp"]
+SOURCES = ["kernels.cu", "ks_tc.cu", "context.cu", "wavefront.cu", "ledger.cpp"]
 
 
 def _headers():

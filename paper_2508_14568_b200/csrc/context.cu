@@ -130,23 +130,54 @@ uint32_t lut_id(lv_ctx* c, const std::array<int32_t, 16>& e) {
 }
 
 // ---------------------------------------------------------------- PBS driver
-void launch_pbs_dev(lv_ctx* c, const LinDesc* d_desc, const uint32_t* d_lut, const BrOut* d_out,
-                    uint32_t count, cudaEvent_t ks_done) {
-  if (!count) return;
+#ifndef LVB_KS_TC
+#define LVB_KS_TC 1
+#endif
+
+// Key switch + modulus switch of `count` items (prologue descriptors d_desc)
+// into d_ms: the tcgen05 i8 GEMM (ks_tc.cu) by default, the CUDA-core
+// kernel with -DLVB_KS_TC=0 (kept for A/B measurement; both bit-exact).
+static void launch_keyswitch(lv_ctx* c, const LinDesc* d_desc, uint32_t count, uint16_t* d_ms,
+                             uint64_t* small_out) {
   const uint32_t stride = ms_stride(c);
-  uint16_t* d_ms = c->ms.get((size_t)count * stride);
-  KsArgs ka{d_desc, c->d_pool, kBigStride, c->d_ksk, c->d_ksk_bias, c->p.n, count, d_ms, stride, nullptr};
   const uint32_t row = c->p.n + 1;
+#if LVB_KS_TC
+  constexpr uint32_t kChunk = 32768;  // items per GEMM launch (grid.y <= 65535 rows)
+  const uint32_t rows_max = (std::min(count, kChunk) + 127) / 128 * 128;
+  uint8_t* dig = c->ks_digits.get((size_t)rows_max * kBig * kKsLevel);
+  uint64_t* body = c->ks_body.get(rows_max);
+  for (uint32_t off = 0; off < count; off += kChunk) {
+    const uint32_t cnt = std::min(count - off, kChunk);
+    const uint32_t mt = (cnt + 127) / 128;
+    ks_digits_kernel<<<dim3((kBig + 1 + 255) / 256, mt * 128), 256, 0, c->stream>>>(
+        d_desc + off, c->d_pool, kBigStride, cnt, dig, body);
+    ks_mma_kernel<<<dim3(ks_tc_ntiles(c->p.n), mt), 128, ks_tc_smem_bytes(), c->stream>>>(
+        dig, c->d_ksk_bt, c->d_ksk_bias, body, c->p.n, cnt, d_ms + (size_t)off * stride, stride,
+        small_out ? small_out + (size_t)off * row : nullptr);
+  }
+#else
+  KsArgs ka{d_desc, c->d_pool, kBigStride, c->d_ksk, c->d_ksk_bias, c->p.n, count, d_ms, stride,
+            small_out};
   for (uint32_t off = 0; off < count; off += 65535u * kKsItems) {
     const uint32_t cnt = std::min<uint32_t>(count - off, 65535u * kKsItems);
     KsArgs k2 = ka;
     k2.desc = d_desc + off;
     k2.count = cnt;
     k2.ms = d_ms + (size_t)off * stride;
+    k2.small_out = small_out ? small_out + (size_t)off * row : nullptr;
     dim3 grid((row + 127) / 128, (cnt + kKsItems - 1) / kKsItems);
     keyswitch_kernel<<<grid, 128, 0, c->stream>>>(k2);
   }
+#endif
   LV_CUDA(cudaGetLastError());
+}
+
+void launch_pbs_dev(lv_ctx* c, const LinDesc* d_desc, const uint32_t* d_lut, const BrOut* d_out,
+                    uint32_t count, cudaEvent_t ks_done) {
+  if (!count) return;
+  const uint32_t stride = ms_stride(c);
+  uint16_t* d_ms = c->ms.get((size_t)count * stride);
+  launch_keyswitch(c, d_desc, count, d_ms, nullptr);
   if (ks_done) LV_CUDA(cudaEventRecord(ks_done, c->stream));
   BrArgs ba{d_ms, stride, d_lut, c->d_tp, c->d_bskf, c->d_tw, c->d_twist, c->p.n,
             c->d_pool, kBigStride, d_out};
@@ -338,6 +369,13 @@ static void keygen(lv_ctx* c) {
   LV_CUDA(cudaMalloc(&c->d_ksk_bias, (size_t)(n + 1) * sizeof(uint64_t)));
   ksk_bias_kernel<<<(n + 1 + 127) / 128, 128, 0, c->stream>>>(c->d_ksk, n, c->d_ksk_bias);
   LV_CUDA(cudaGetLastError());
+  {
+    const uint32_t rows = ks_tc_ntiles(n) * 32 * 8;  // limb rows, zero-padded past n
+    LV_CUDA(cudaMalloc(&c->d_ksk_bt, (size_t)rows * kBig * kKsLevel));
+    ksk_limbs_kernel<<<dim3((kBig * kKsLevel + 255) / 256, rows / 8), 256, 0, c->stream>>>(
+        c->d_ksk, n, c->d_ksk_bt);
+    LV_CUDA(cudaGetLastError());
+  }
   uint64_t* d_bsk = nullptr;
   LV_CUDA(cudaMalloc(&d_bsk, (size_t)n * kRows * (kK + 1) * kN * sizeof(uint64_t)));
   keygen_bsk_kernel<<<n * kRows, 256, 0, c->stream>>>(c->seed, c->p.glwe_noise_log2, c->d_sk_small,
@@ -424,6 +462,8 @@ int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
       LV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       LV_CUDA(cudaFuncSetAttribute(blind_rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)blind_rotate_smem_bytes(p.n)));
+      LV_CUDA(cudaFuncSetAttribute(ks_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)ks_tc_smem_bytes()));
       build_tables(c);
       keygen(c);
       c->min_lut[0] = lut_id(c, min_lut_entries(false));
@@ -454,6 +494,9 @@ void lv_ctx_destroy(lv_ctx* c) {
   c->u32a.release();
   c->u32b.release();
   c->i32a.release();
+  c->ks_digits.release();
+  c->ks_body.release();
+  if (c->d_ksk_bt) cudaFree(c->d_ksk_bt);
   c->u64a.release();
   c->u64b.release();
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -736,10 +779,7 @@ int lv_debug_keyswitch(lv_ctx* c, const uint64_t* in, size_t count, uint64_t* ou
     const uint32_t row = c->p.n + 1, stride = ms_stride(c);
     uint64_t* dsmall = c->u64b.get(count * row);
     uint16_t* dms = c->ms.get(count * stride);
-    KsArgs ka{dd, c->d_pool, kBigStride, c->d_ksk, c->d_ksk_bias, c->p.n, (uint32_t)count, dms, stride, dsmall};
-    dim3 grid((row + 127) / 128, (uint32_t)((count + kKsItems - 1) / kKsItems));
-    keyswitch_kernel<<<grid, 128, 0, c->stream>>>(ka);
-    LV_CUDA(cudaGetLastError());
+    launch_keyswitch(c, dd, (uint32_t)count, dms, dsmall);
     LV_CUDA(cudaMemcpyAsync(out_small, dsmall, count * row * 8, cudaMemcpyDeviceToHost, c->stream));
     LV_CUDA(cudaStreamSynchronize(c->stream));
     pool_free(c, s.data(), count);

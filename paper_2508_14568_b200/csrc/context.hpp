@@ -103,6 +103,10 @@ struct lv_ctx {
   lvb::DevBuf<uint32_t> u32a, u32b;
   lvb::DevBuf<int32_t> i32a;
   lvb::DevBuf<uint64_t> u64a, u64b;
+  // tensor-core key switch: KSK byte limbs (transposed, K-major), digits, bodies
+  uint8_t* d_ksk_bt = nullptr;
+  lvb::DevBuf<uint8_t> ks_digits;
+  lvb::DevBuf<uint64_t> ks_body;
 
   std::map<std::string, lvb::PairPlan> plan_cache;
   uint32_t min_lut[2] = {0, 0};

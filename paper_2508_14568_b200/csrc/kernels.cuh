@@ -125,3 +125,15 @@ void set_twist_coarse(const double2* host8);
 constexpr int kKsItems = 32;
 
 }  // namespace lvb
+
+namespace lvb {
+// tensor-core key switch (ks_tc.cu)
+__global__ void ks_digits_kernel(const LinDesc* desc, const uint64_t* pool, uint32_t pool_stride,
+                                 uint32_t count, uint8_t* digits, uint64_t* body);
+__global__ void ksk_limbs_kernel(const uint64_t* ksk, uint32_t n, uint8_t* bt);
+__global__ void ks_mma_kernel(const uint8_t* digits, const uint8_t* bt, const uint64_t* bias,
+                              const uint64_t* body, uint32_t n, uint32_t count, uint16_t* ms,
+                              uint32_t ms_stride, uint64_t* small_out);
+size_t ks_tc_smem_bytes();
+uint32_t ks_tc_ntiles(uint32_t n);
+}  // namespace lvb

@@ -270,7 +270,11 @@ static void run_traversals(lv_ctx* c, const std::vector<PairIn>& pairs, uint32_t
     LV_CUDA(cudaMemcpyAsync(dout, o.data(), o.size() * sizeof(BrOut), cudaMemcpyHostToDevice, c->stream));
     size_t max_wave = 0;
     for (const Launch& L : launches) max_wave = std::max(max_wave, L.count);
-    c->ms.get(max_wave * ms_stride(c));  // size scratch before capture
+    // size every scratch buffer before capture (no allocation inside a graph)
+    c->ms.get(max_wave * ms_stride(c));
+    const size_t ks_rows = (std::min<size_t>(max_wave, 32768) + 127) / 128 * 128;
+    c->ks_digits.get(ks_rows * kBig * kKsLevel);
+    c->ks_body.get(ks_rows);
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     LV_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
