@@ -760,8 +760,8 @@ int lv_debug_keys(lv_ctx* c, uint8_t* sk_small, uint8_t* sk_glwe, uint64_t* ksk,
               for (uint32_t t = 0; t < 128; ++t) {
                 const double2 v = raw[i * 4096 + (q * 4 + r * 2 + o) * 128 + t];
                 const size_t base = ((i * kRows + r) * (kK + 1) + o) * 2 * kM + 2 * (8 * t + q);
-                bskf_nat[base] = v.x;
-                bskf_nat[base + 1] = v.y;
+                bskf_nat[base] = v.x * 1024.0;  // undo the exact 2^-10 pre-scaling
+                bskf_nat[base + 1] = v.y * 1024.0;
               }
     }
   });

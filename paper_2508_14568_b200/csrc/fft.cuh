@@ -47,6 +47,10 @@ constexpr int kXchgBufs = kSplitXchg ? 1 : 2;
 // guarantees the buffer is free on entry.
 template <int P, typename WR, typename RD>
 __device__ __forceinline__ void xchg(double2 (&X)[P][8], double2* buf, WR wr, RD rd) {
+#ifdef LVB_ABL_XCHG  // timing ablation only: results are wrong
+  __syncthreads();
+  return;
+#endif
   if constexpr (!kSplitXchg || P == 1) {
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -117,6 +121,9 @@ __device__ __forceinline__ void dit1(double2& p, double2& q) {  // w = W[0]
 // concatenated: T_s starts at kM - (kM >> s). Same values as W, laid out so
 // every warp-wide twiddle load is contiguous.
 __device__ __forceinline__ double2 tws(const double2* __restrict__ tw, int s, uint32_t y) {
+#ifdef LVB_ABL_TW  // timing ablation only
+  return make_double2(0.70710678118654757 + s * 1e-3, 0.70710678118654757 - y * 1e-9);
+#endif
   return __ldg(tw + (kM - (kM >> s)) + y);
 }
 
@@ -341,14 +348,126 @@ __device__ __forceinline__ void fft_inverse(double2 (&X)[P][8], double2* buf,
   }
 }
 
+// ------------------------------------------------ inverse, natural layout A
+// Same arithmetic as fft_inverse (DIT stages 9..0), different data path:
+//   stages 9,8,7 on the thread's bins 8t + r            (registers)
+//   -> B' (t = 8b + u, x = 64b + u + 8r): stages 6,5,4  (shared exchange)
+//   stage 3 (pairs x, x+64 in lanes t, t^8)             (shfl.xor 8)
+//   -> A  (x = t + 128 r): stages 2,1,0                 (shared exchange)
+// so the output lands in the layout fft_forward's input uses: each thread
+// owns the same accumulator coefficients in both halves of a CMUX.
+template <int P>
+__device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
+                                              const double2* __restrict__ tw, uint32_t t) {
+  {
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int r = 0; r < 8; r += 2) dit1(X[p][r], X[p][r + 1]);
+    const double2 w81 = tws(tw, 8, 1);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      dit1(X[p][0], X[p][2]);
+      dit(X[p][1], X[p][3], w81);
+      dit1(X[p][4], X[p][6]);
+      dit(X[p][5], X[p][7], w81);
+    }
+    const double2 w71 = tws(tw, 7, 1), w72 = tws(tw, 7, 2), w73 = tws(tw, 7, 3);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      dit1(X[p][0], X[p][4]);
+      dit(X[p][1], X[p][5], w71);
+      dit(X[p][2], X[p][6], w72);
+      dit(X[p][3], X[p][7], w73);
+    }
+  }
+  const uint32_t b = t >> 3, u = t & 7, odd = b & 1;
+  xchg<P>(X, buf, [&](int r) { return 8 * t + r; }, [&](int r) { return 64 * b + u + 8 * r; });
+  {
+    const double2 w6 = tws(tw, 6, u);
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w6);
+    const double2 w50 = tws(tw, 5, u), w51 = tws(tw, 5, u + 8);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      dit(X[p][0], X[p][2], w50);
+      dit(X[p][1], X[p][3], w51);
+      dit(X[p][4], X[p][6], w50);
+      dit(X[p][5], X[p][7], w51);
+    }
+    double2 w4[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) w4[r] = tws(tw, 4, u + 8 * r);
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) dit(X[p][r], X[p][r + 4], w4[r]);
+    // stage 3 (half 64): even b holds x, odd b holds x + 64; even lane
+    // finishes r = 0..3, odd lane r = 4..7
+    double2 w3[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w3[q] = tws(tw, 3, u + 8 * (q + 4 * odd));
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      double2 Y[4];
+      // even lane needs the odd lane's X[q] (upper of r=q); odd lane needs
+      // the even lane's X[4+q] (lower of r=4+q)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Y[q] = shfl_xor_d2(odd ? X[p][q] : X[p][4 + q], 8);
+      double2 Z[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double2 lo = odd ? Y[q] : X[p][q];
+        double2 hi = odd ? X[p][4 + q] : Y[q];
+        dit(lo, hi, w3[q]);
+        Z[q] = lo;
+        Z[4 + q] = hi;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) X[p][q] = Z[q];
+    }
+  }
+  __syncthreads();
+  xchg<P>(
+      X, buf,
+      [&](int r) { return 64 * (b & ~1u) + u + 8 * ((r & 3) + 4 * odd) + 64 * (r >> 2); },
+      [&](int r) { return t + 128 * r; });
+  {
+    const double2 w2 = tws(tw, 2, t);
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w2);
+    const double2 w10 = tws(tw, 1, t), w11 = tws(tw, 1, t + 128);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      dit(X[p][0], X[p][2], w10);
+      dit(X[p][1], X[p][3], w11);
+      dit(X[p][4], X[p][6], w10);
+      dit(X[p][5], X[p][7], w11);
+    }
+    double2 w0[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) w0[r] = tws(tw, 0, t + 128 * r);
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) dit(X[p][r], X[p][r + 4], w0[r]);
+  }
+}
+
 // f64 -> Z_{2^64}, identical to oracle f64_to_torus. (An integer-pipe
 // variant — exponent/mantissa shift for |y| >= 2^52 — measured slower on
 // B200, 87-90 ms vs 82.5 ms per 4096 PBS, and was dropped.)
+// Here r = floor(y 2^-64 + 1/2) (exact: |y 2^-64| < 2^32, so the sum keeps
+// every bit) differs from the oracle's rint only on exact ties, where it
+// yields d = -2^63 instead of +2^63 - 2^64 — the same residue — so no tie
+// fix-up is needed, and d = y - r 2^64 is one exact FMA.
 __device__ __forceinline__ uint64_t f64_to_torus(double y) {
-  const double two64 = 18446744073709551616.0;
-  const double r = rint(__dmul_rn(y, 0x1p-64));
-  double d = __dsub_rn(y, __dmul_rn(r, two64));
-  if (d >= 9223372036854775808.0) d = __dsub_rn(d, two64);
+  const double r = floor(__dadd_rn(__dmul_rn(y, 0x1p-64), 0.5));
+  const double d = __fma_rn(-r, 18446744073709551616.0, y);
   return (uint64_t)__double2ll_rn(d);
 }
 

@@ -25,6 +25,9 @@ void set_twist_coarse(const double2* host8) {
 // Streaming read of the Fourier BSK: no L1 allocation, so the twiddle tables
 // stay resident in L1 (the BSK itself is L2-resident, 57.7 MB < 126 MB).
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
+#ifdef LVB_ABL_BSK  // timing ablation only
+  return make_double2(1.0 + (double)((uintptr_t)p & 0xff), 0.5);
+#endif
   double2 v;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
                : "=d"(v.x), "=d"(v.y) : "l"(p));
@@ -38,8 +41,11 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
 //
 // Shared memory: acc[2][N] u64 (32 KB) + FFT exchange buffer kXchgBufs x kM
 // double2 (16 KB split / 32 KB) + ms[n+1] u16.
+#ifndef LVB_OWN_ACC
+#define LVB_OWN_ACC 2
+#endif
 #ifndef LVB_BR_MIN_BLOCKS
-#define LVB_BR_MIN_BLOCKS 4
+#define LVB_BR_MIN_BLOCKS (LVB_OWN_ACC ? 3 : 4)
 #endif
 __global__ void __launch_bounds__(128, LVB_BR_MIN_BLOCKS)
 blind_rotate_kernel(BrArgs a) {
@@ -69,6 +75,23 @@ blind_rotate_kernel(BrArgs a) {
   const double2* __restrict__ tw = a.twiddles;
   const double2* __restrict__ twist = a.twist;
 
+#if LVB_OWN_ACC
+  // Thread t owns accumulator coefficients t + 128 r (+ 1024) of both
+  // polynomials: the forward FFT reads them there and fft_inverse_a writes
+  // the external product there, so they live in registers across the
+  // top-of-loop barrier; shared memory only serves the rotated reads.
+  __syncthreads();
+  uint64_t own[2][16];  // [poly][2 r + half]
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      own[p][2 * r] = acc[p * kN + t + 128 * r];
+      own[p][2 * r + 1] = acc[p * kN + t + 128 * r + kM];
+    }
+  const double2 tw_fine = __ldg(twist + t);  // twist of x = t + 128 r is fine[t] * coarse[r]
+#endif
+
   for (uint32_t i = 0; i < n; ++i) {
     __syncthreads();
     const uint32_t rot = ms[i];
@@ -89,9 +112,18 @@ blind_rotate_kernel(BrArgs a) {
           const uint32_t s = (j + 2 * kN - rot) & (2 * kN - 1);
           const uint64_t pv = P[s & (kN - 1)];  // one load; the wrap only flips the sign
           const uint64_t rv = s < kN ? pv : (uint64_t)0 - pv;
+#if LVB_OWN_ACC
+          d[hpart] = (int32_t)decomp1(rv - own[p][2 * r + hpart], kPbsBaseLog);
+#else
           d[hpart] = (int32_t)decomp1(rv - P[j], kPbsBaseLog);
+#endif
         }
+#if LVB_OWN_ACC
+        const double2 tz = r == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]);
+        X[p][r] = cmul(make_double2((double)d[0], (double)d[1]), tz);
+#else
         X[p][r] = cmul(make_double2((double)d[0], (double)d[1]), twist_at(twist, x));
+#endif
       }
     }
 
@@ -129,6 +161,31 @@ blind_rotate_kernel(BrArgs a) {
       }
     }
     __syncthreads();  // forward's last buffer reads precede the inverse's writes
+#if LVB_OWN_ACC
+    fft_inverse_a<2>(X, buf, tw, t);
+    // untwist (conj(twist) / M, exact scaling), back to the torus, accumulate
+    // into the owned coefficients and publish them for the next rotation
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const double2 tv = r == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]);
+      const double2 ut = make_double2(tv.x, -tv.y);  // the 1/M is pre-applied to the BSK
+      const uint32_t x = t + 128 * r;
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const double2 z = cmul(X[p][r], ut);
+#if LVB_OWN_ACC == 2
+        // re-read (unchanged during the CMUX) instead of holding 64 registers
+        // across the FFTs; owned only from here to the next rotation
+        own[p][2 * r] = acc[p * kN + x];
+        own[p][2 * r + 1] = acc[p * kN + x + kM];
+#endif
+        own[p][2 * r] += f64_to_torus(z.x);
+        own[p][2 * r + 1] += f64_to_torus(z.y);
+        acc[p * kN + x] = own[p][2 * r];
+        acc[p * kN + x + kM] = own[p][2 * r + 1];
+      }
+    }
+#else
     fft_inverse<2>(X, buf, tw, t);
 
     // untwist, back to the torus, accumulate
@@ -141,7 +198,7 @@ blind_rotate_kernel(BrArgs a) {
           const uint32_t x = u + 64 * (4 * h + q) + 512 * hi;
           // untwist = conj(twist) / M (exact power-of-two scaling)
           const double2 tv = twist_at(twist, x);
-          const double2 ut = make_double2(__dmul_rn(tv.x, 0x1p-10), __dmul_rn(-tv.y, 0x1p-10));
+          const double2 ut = make_double2(tv.x, -tv.y);  // the 1/M is pre-applied to the BSK
 #pragma unroll
           for (int p = 0; p < 2; ++p) {
             const double2 z = cmul(X[p][4 * hi + q], ut);
@@ -151,6 +208,7 @@ blind_rotate_kernel(BrArgs a) {
         }
       }
     }
+#endif
   }
   __syncthreads();
 
@@ -450,7 +508,10 @@ bsk_fourier_kernel(const uint64_t* bsk, const double2* __restrict__ tw,
   for (int q = 0; q < 8; ++q)
 #pragma unroll
     for (int o = 0; o < 2; ++o)
-      bskf[(size_t)i * (32 * 128) + (q * 4 + r * 2 + o) * 128 + t] = X[o][q];
+      // stored pre-scaled by 1/M = 2^-10 (exact): the untwist then needs no
+      // scaling multiply and every rounding downstream is unchanged
+      bskf[(size_t)i * (32 * 128) + (q * 4 + r * 2 + o) * 128 + t] =
+          make_double2(__dmul_rn(X[o][q].x, 0x1p-10), __dmul_rn(X[o][q].y, 0x1p-10));
 }
 
 // Debug / parity entry: forward transform of one integer polynomial, output
