@@ -173,9 +173,10 @@ int lv_debug_keys(lv_ctx* ctx, uint8_t* sk_small, uint8_t* sk_glwe, uint64_t* ks
 /* Key switch only: count big LWE rows -> count small LWE rows (n+1 u64). */
 int lv_debug_keyswitch(lv_ctx* ctx, const uint64_t* in, size_t count, uint64_t* out_small);
 /* Blind rotation only, from modulus-switched inputs (count rows of n+1 u32)
- * -> extracted big LWE rows. */
+ * -> extracted big LWE rows; glwe_out (nullable) also receives the whole
+ * accumulator, count x (k+1) x N u64 (phase-noise measurements). */
 int lv_debug_blind_rotate(lv_ctx* ctx, const uint32_t* ms, const uint32_t* lut_ids,
-                          size_t count, uint64_t* out);
+                          size_t count, uint64_t* out, uint64_t* glwe_out);
 int lv_debug_fft(lv_ctx* ctx, const int64_t* poly, double* spec, uint64_t* roundtrip);
 
 /* ---- timing helpers for bench.py (device-resident workloads) ----------- */

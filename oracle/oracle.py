@@ -78,6 +78,8 @@ def lib():
         L.orc_test_poly.argtypes = [vp, i32p, u64p]
         L.orc_blind_rotate.argtypes = [vp, u32p, u64p, u64p, ctypes.c_int]
         L.orc_sample_extract.argtypes = [vp, u64p, u64p]
+        L.orc_blind_rotate_batch.argtypes = [vp, ctypes.c_size_t, u32p, u64p, u64p, ctypes.c_int,
+                                             ctypes.c_int]
         L.orc_pbs.argtypes = [vp, u64p, i32p, u64p, ctypes.c_int]
         L.orc_pbs_batch.argtypes = [vp, ctypes.c_size_t, u64p, i32p, u64p, ctypes.c_int, ctypes.c_int]
         L.orc_fft_forward_i64.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double)]
@@ -183,6 +185,14 @@ class Oracle:
         out = np.zeros((self.k + 1) * self.N, np.uint64)
         lib().orc_blind_rotate(self._c, _p(ms, ctypes.c_uint32), _p(tp, ctypes.c_uint64),
                                _p(out, ctypes.c_uint64), mode)
+        return out
+
+    def blind_rotate_batch(self, ms: np.ndarray, tp: np.ndarray, mode: int = 0, threads: int = 0):
+        ms = np.ascontiguousarray(ms, np.uint32).reshape(-1, self.n + 1)
+        tp = np.ascontiguousarray(tp, np.uint64)
+        out = np.zeros((ms.shape[0], (self.k + 1) * self.N), np.uint64)
+        lib().orc_blind_rotate_batch(self._c, ms.shape[0], _p(ms, ctypes.c_uint32),
+                                     _p(tp, ctypes.c_uint64), _p(out, ctypes.c_uint64), mode, threads)
         return out
 
     def sample_extract(self, glwe: np.ndarray) -> np.ndarray:

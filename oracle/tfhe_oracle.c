@@ -675,3 +675,23 @@ void orc_pbs_batch(const orc_ctx* c, size_t count, const uint64_t* in, const int
   pbs_batch_arg a = {c, in, luts, out, mode};
   parallel_for(count, threads, pbs_range, &a);
 }
+
+typedef struct {
+  const orc_ctx* c;
+  const uint32_t* ms;
+  const uint64_t* tp;
+  uint64_t* out;
+  int mode;
+} br_batch_arg;
+
+static void br_range(void* a, size_t lo, size_t hi) {
+  br_batch_arg* b = (br_batch_arg*)a;
+  const size_t n1 = b->c->p.n + 1, g = (size_t)(b->c->p.k + 1) * b->c->p.N;
+  for (size_t t = lo; t < hi; ++t) orc_blind_rotate(b->c, b->ms + t * n1, b->tp, b->out + t * g, b->mode);
+}
+
+void orc_blind_rotate_batch(const orc_ctx* c, size_t count, const uint32_t* ms,
+                            const uint64_t* tp, uint64_t* glwe_out, int mode, int threads) {
+  br_batch_arg a = {c, ms, tp, glwe_out, mode};
+  parallel_for(count, threads, br_range, &a);
+}

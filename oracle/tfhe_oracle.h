@@ -88,6 +88,9 @@ void orc_test_poly(const orc_ctx* c, const int32_t lut[16], uint64_t* tp);
 void orc_blind_rotate(const orc_ctx* c, const uint32_t* ms, const uint64_t* tp,
                       uint64_t* glwe_out, int mode);
 void orc_sample_extract(const orc_ctx* c, const uint64_t* glwe, uint64_t* out_big);
+/* count blind rotations (ms rows of n+1, one test polynomial) over threads. */
+void orc_blind_rotate_batch(const orc_ctx* c, size_t count, const uint32_t* ms,
+                            const uint64_t* tp, uint64_t* glwe_out, int mode, int threads);
 
 /* Whole PBS: KS -> MS -> BR -> SE. */
 void orc_pbs(const orc_ctx* c, const uint64_t* in_big, const int32_t lut[16],

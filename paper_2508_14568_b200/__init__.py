@@ -181,7 +181,7 @@ def lib():
             "lv_debug_keys": (ctypes.c_int, [vp, P(ctypes.c_uint8), P(ctypes.c_uint8), P(u64),
                                              P(ctypes.c_double)]),
             "lv_debug_keyswitch": (ctypes.c_int, [vp, P(u64), sz, P(u64)]),
-            "lv_debug_blind_rotate": (ctypes.c_int, [vp, P(u32), P(u32), sz, P(u64)]),
+            "lv_debug_blind_rotate": (ctypes.c_int, [vp, P(u32), P(u32), sz, P(u64), P(u64)]),
             "lv_debug_fft": (ctypes.c_int, [vp, P(i64), P(ctypes.c_double), P(u64)]),
             "lv_bench_pbs": (ctypes.c_int, [vp, P(u32), P(u32), sz, ctypes.c_int, u64,
                                             P(ctypes.c_float), P(ctypes.c_float),
@@ -427,13 +427,15 @@ class Context:
                                         _ptr(out, ctypes.c_uint64)))
         return out
 
-    def debug_blind_rotate(self, ms, lut_ids):
+    def debug_blind_rotate(self, ms, lut_ids, glwe: bool = False):
         m = np.ascontiguousarray(ms, np.uint32).reshape(-1, self.n + 1)
         ids = _u32(lut_ids)
         out = np.zeros((m.shape[0], self.row), np.uint64)
+        g = np.zeros((m.shape[0], 2 * self.N), np.uint64) if glwe else None
         _check(lib().lv_debug_blind_rotate(self._h, _ptr(m, ctypes.c_uint32), _ptr(ids, ctypes.c_uint32),
-                                           m.shape[0], _ptr(out, ctypes.c_uint64)))
-        return out
+                                           m.shape[0], _ptr(out, ctypes.c_uint64),
+                                           _ptr(g, ctypes.c_uint64) if glwe else None))
+        return (out, g) if glwe else out
 
     def debug_fft(self, poly):
         p = np.ascontiguousarray(poly, np.int64)

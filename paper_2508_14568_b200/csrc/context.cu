@@ -66,6 +66,9 @@ std::vector<lv_ct> pool_alloc(lv_ctx* c, size_t count) {
     c->live[out[i]] = 1;
     c->ledgers[out[i]] = NoiseLedger();
   }
+  // ascending slots: batches recycled through the LIFO free list come back
+  // as long contiguous runs, so host<->device row copies stay one 2D copy
+  std::sort(out.begin(), out.end());
   return out;
 }
 
@@ -787,7 +790,7 @@ int lv_debug_keyswitch(lv_ctx* c, const uint64_t* in, size_t count, uint64_t* ou
 }
 
 int lv_debug_blind_rotate(lv_ctx* c, const uint32_t* ms, const uint32_t* luts, size_t count,
-                          uint64_t* out) {
+                          uint64_t* out, uint64_t* glwe_out) {
   return guard([&] {
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     const uint32_t row = c->p.n + 1, stride = ms_stride(c);
@@ -805,10 +808,18 @@ int lv_debug_blind_rotate(lv_ctx* c, const uint32_t* ms, const uint32_t* luts, s
     LV_CUDA(cudaMemcpyAsync(dout, o.data(), count * sizeof(BrOut), cudaMemcpyHostToDevice, c->stream));
     BrArgs ba{dms, stride, dl, c->d_tp, c->d_bskf, c->d_tw, c->d_twist, c->p.n,
               c->d_pool, kBigStride, dout};
+    uint64_t* dglwe = nullptr;
+    if (glwe_out) {
+      LV_CUDA(cudaMalloc(&dglwe, count * 2 * kN * sizeof(uint64_t)));
+      ba.glwe_out = dglwe;
+    }
     blind_rotate_kernel<<<(uint32_t)count, 128, blind_rotate_smem_bytes(c->p.n), c->stream>>>(ba);
     LV_CUDA(cudaGetLastError());
     download_rows(c, s, out);
+    if (dglwe)
+      LV_CUDA(cudaMemcpyAsync(glwe_out, dglwe, count * 2 * kN * 8, cudaMemcpyDeviceToHost, c->stream));
     LV_CUDA(cudaStreamSynchronize(c->stream));
+    if (dglwe) cudaFree(dglwe);
     pool_free(c, s.data(), count);
   });
 }

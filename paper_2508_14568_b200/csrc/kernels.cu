@@ -212,6 +212,9 @@ blind_rotate_kernel(BrArgs a) {
   }
   __syncthreads();
 
+  if (a.glwe_out)  // debug / noise measurement: the whole accumulator
+    for (uint32_t j = t; j < 2 * kN; j += 128) a.glwe_out[(size_t)item * 2 * kN + j] = acc[j];
+
   // sample extract coefficient 0 (a'_0 = A_0, a'_j = -A_{N-j}, b' = B_0) + epilogue
   const BrOut o = a.outs[item];
   const uint32_t S = a.pool_stride;

@@ -56,6 +56,7 @@ struct BrArgs {
   uint64_t* pool;              // pool base
   uint32_t pool_stride;
   const BrOut* outs;           // [count]
+  uint64_t* glwe_out = nullptr;  // debug: full accumulator [count][2][N] (noise tests)
 };
 
 struct KsArgs {
