@@ -175,15 +175,30 @@ static void run_traversals(lv_ctx* c, const std::vector<PairIn>& pairs, uint32_t
     const PairIn& in = pairs[p];
     const PairPlan& plan = *plans[p];
     lv_run r{};
+    // Equality slots live from stage 0 (wave k-2) to the cell (wave k-2+S):
+    // diagonals k and k+S+1 never overlap, so a ring of S+1 diagonal groups
+    // (each up to min(m,n) cells x S slots) serves the whole traversal.
+    const size_t diag_cap = (size_t)std::min(in.m, in.n) + 1;
+    std::vector<lv_ct> ring;
+    if (S > 0) {
+      ring = pool_alloc(c, (S + 1) * diag_cap * S);
+      temps.insert(temps.end(), ring.begin(), ring.end());
+    }
+    int64_t cur_k = -1;
+    size_t idx_in_diag = 0;
     for (const CellPlan& cell : plan.cells) {
       const int64_t k = (int64_t)cell.i + cell.j;
       const int64_t wcell = k - 2 + S;
+      if (k != cur_k) {
+        cur_k = k;
+        idx_in_diag = 0;
+      }
+      const size_t cell_in_diag = idx_in_diag++;
       lv_ct eq9;
       if (S > 0) {
         const lv_ct* ai = in.a + (size_t)(cell.i - 1) * S;
         const lv_ct* bj = in.b + (size_t)(cell.j - 1) * S;
-        std::vector<lv_ct> eqs = pool_alloc(c, S);
-        temps.insert(temps.end(), eqs.begin(), eqs.end());
+        const lv_ct* eqs = ring.data() + ((size_t)(k % (S + 1)) * diag_cap + cell_in_diag) * S;
         for (uint32_t s = 0; s < S; ++s) {
           PbsItem it{};
           if (s == 0)
