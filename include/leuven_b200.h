@@ -154,6 +154,15 @@ int lv_eq_table_build(lv_ctx* ctx, const lv_ct* a, size_t m, uint32_t symbols,
                       const char* chars, const int32_t* char_symbols, size_t rows,
                       lv_eqtable** out, uint64_t* build_pbs);
 int lv_eq_table_lookup(lv_ctx* ctx, const lv_eqtable* t, char c, uint64_t position, lv_ct* out);
+/* LEQT v2 container (the reference's v1, preprocess.cpp:80-194, with real
+ * LWE rows): meta = the caller's alphabet section, stored verbatim. Pass
+ * buf = NULL to get the size. Loading checks magic/version (FormatError),
+ * truncation (FormatError) and that the rows were encrypted under this
+ * context's keyset (InvalidParams); ledgers get fresh source ids. */
+int lv_eq_table_serialize(lv_ctx* ctx, const lv_eqtable* t, const uint8_t* meta, uint64_t meta_len,
+                          uint8_t* buf, uint64_t cap, uint64_t* len);
+int lv_eq_table_deserialize(lv_ctx* ctx, const uint8_t* buf, uint64_t len, lv_eqtable** out,
+                            uint8_t* meta_out, uint64_t meta_cap, uint64_t* meta_len);
 void lv_eq_table_destroy(lv_ctx* ctx, lv_eqtable* t);
 /* preprocess::distance_preprocessed (preprocess.cpp:62-76). */
 int lv_edit_distance_pre(lv_ctx* ctx, const lv_eqtable* t, const char* plain, size_t n,

@@ -503,6 +503,125 @@ void lv_eq_table_destroy(lv_ctx* c, lv_eqtable* t) {
   delete t;
 }
 
+// LEQT v2: the reference's table container (preprocess.cpp:80-194, v1 held
+// simulated values + ledgers) with real ciphertexts. Little-endian:
+//   "LEQT" u32 version=2 | u32 meta_len, meta (caller's alphabet section) |
+//   u32 n, u32 N, u32 k, u64 key seed (the keyset the rows decrypt under) |
+//   u64 length | u32 rows | rows x { u8 char | length x { u32 terms,
+//   i32 coeff[terms] (ledger, ids rebased on load), u64 lwe[N+1] } }
+}  // extern "C"
+static void put(std::vector<uint8_t>& b, const void* p, size_t n) {
+  const uint8_t* s = (const uint8_t*)p;
+  b.insert(b.end(), s, s + n);
+}
+template <typename T>
+static void put(std::vector<uint8_t>& b, T v) {
+  put(b, &v, sizeof(T));
+}
+extern "C" {
+
+int lv_eq_table_serialize(lv_ctx* c, const lv_eqtable* t, const uint8_t* meta, uint64_t meta_len,
+                          uint8_t* buf, uint64_t cap, uint64_t* len) {
+  return guard_wf([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    std::vector<uint8_t> b;
+    put(b, "LEQT", 4);
+    put<uint32_t>(b, 2);
+    put<uint32_t>(b, (uint32_t)meta_len);
+    if (meta_len) put(b, meta, meta_len);
+    put<uint32_t>(b, c->p.n);
+    put<uint32_t>(b, c->p.N);
+    put<uint32_t>(b, c->p.k);
+    put<uint64_t>(b, c->seed);
+    put<uint64_t>(b, t->length);
+    put<uint32_t>(b, (uint32_t)t->rows.size());
+    std::vector<uint64_t> rows(t->length * (kBig + 1));
+    for (const auto& kv : t->rows) {
+      put<uint8_t>(b, (uint8_t)kv.first);
+      if (t->length) {
+        check_handles(c, kv.second.data(), kv.second.size());
+        LV_CUDA(cudaStreamSynchronize(c->stream));
+        if (int rc = lv_export(c, kv.second.data(), kv.second.size(), rows.data()))
+          throw Error(rc, lv_last_error());
+      }
+      for (uint64_t i = 0; i < t->length; ++i) {
+        const auto& terms = c->ledgers[kv.second[i]].terms();
+        put<uint32_t>(b, (uint32_t)terms.size());
+        for (const auto& term : terms) put<int32_t>(b, term.second);
+        put(b, rows.data() + i * (kBig + 1), (kBig + 1) * 8);
+      }
+    }
+    *len = b.size();
+    if (buf) {
+      if (cap < b.size()) throw Error(LV_ERR_INVALID_PARAMS, "serialize buffer too small");
+      std::memcpy(buf, b.data(), b.size());
+    }
+  });
+}
+
+int lv_eq_table_deserialize(lv_ctx* c, const uint8_t* buf, uint64_t len, lv_eqtable** out,
+                            uint8_t* meta_out, uint64_t meta_cap, uint64_t* meta_len) {
+  return guard_wf([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    uint64_t pos = 0;
+    auto take = [&](void* dst, uint64_t n) {
+      if (pos + n > len) throw Error(LV_ERR_FORMAT, "truncated table file");
+      if (dst) std::memcpy(dst, buf + pos, n);
+      pos += n;
+    };
+    auto get32 = [&] { uint32_t v; take(&v, 4); return v; };
+    auto get64 = [&] { uint64_t v; take(&v, 8); return v; };
+    char magic[4];
+    take(magic, 4);
+    if (std::memcmp(magic, "LEQT", 4) != 0) throw Error(LV_ERR_FORMAT, "not an equality-table file");
+    const uint32_t version = get32();
+    if (version != 2)
+      throw Error(LV_ERR_FORMAT, "unsupported table version " + std::to_string(version));
+    const uint32_t ml = get32();
+    if (meta_len) *meta_len = ml;
+    if (ml > len - pos) throw Error(LV_ERR_FORMAT, "truncated table file");
+    if (meta_out && ml <= meta_cap) std::memcpy(meta_out, buf + pos, ml);
+    pos += ml;
+    const uint32_t n = get32(), N = get32(), k = get32();
+    const uint64_t seed = get64();
+    if (n != c->p.n || N != c->p.N || k != c->p.k || seed != c->seed)
+      throw Error(LV_ERR_INVALID_PARAMS, "table was encrypted under a different keyset");
+    const uint64_t length = get64();
+    const uint32_t nrows = get32();
+    auto* t = new lv_eqtable();
+    t->length = length;
+    try {
+      std::vector<uint64_t> rows(length * (kBig + 1));
+      for (uint32_t r = 0; r < nrows; ++r) {
+        uint8_t ch;
+        take(&ch, 1);
+        std::vector<std::vector<int32_t>> coeffs(length);
+        for (uint64_t i = 0; i < length; ++i) {
+          const uint32_t terms = get32();
+          if ((uint64_t)terms * 4 > len - pos) throw Error(LV_ERR_FORMAT, "truncated table file");
+          coeffs[i].resize(terms);
+          if (terms) take(coeffs[i].data(), (uint64_t)terms * 4);
+          take(rows.data() + i * (kBig + 1), (kBig + 1) * 8);
+        }
+        std::vector<lv_ct> slots(length);
+        if (length)
+          if (int rc = lv_import(c, rows.data(), length, slots.data())) throw Error(rc, lv_last_error());
+        for (uint64_t i = 0; i < length; ++i) {  // fresh source ids (reserve_source_ids)
+          NoiseLedger led;
+          for (int32_t co : coeffs[i]) led.add_scaled(NoiseLedger::fresh(c->next_source++), co);
+          c->ledgers[slots[i]] = std::move(led);
+        }
+        if (t->rows.count((char)ch)) throw Error(LV_ERR_FORMAT, "duplicate table row");
+        t->rows[(char)ch] = std::move(slots);
+      }
+    } catch (...) {
+      lv_eq_table_destroy(c, t);
+      throw;
+    }
+    *out = t;
+  });
+}
+
 int lv_edit_distance_pre(lv_ctx* c, const lv_eqtable* t, const char* plain, size_t n,
                          const lv_band* band, int32_t key_encoding, lv_ct* score, lv_run* run) {
   return guard_wf([&] {

@@ -376,3 +376,161 @@ def compute_batch(pairs, encoding: str = "ascii7", budget: float = 4000.0,
             if t.size:
                 ctx.release(t)
     return out
+
+
+# ------------------------------------------------------------ RunReport / batch
+REPORT_FIELDS = ["distance", "mode", "half_width", "visited_cells", "pbs_total", "pbs_equality",
+                 "pbs_kernel", "refresh_count", "preprocessing_pbs", "max_key_variance"]
+
+
+def report_json(report: dict, include_timing: bool = False) -> str:
+    """cli::report_json (cli.cpp:93-107): compact, field order fixed, timing
+    excluded from batch lines so equal inputs serialise to equal bytes."""
+    import json
+    obj = {k: report[k] for k in REPORT_FIELDS}
+    if include_timing:
+        obj["wall_time_ms"] = report["wall_time_ms"]
+    return json.dumps(obj, separators=(",", ":"))
+
+
+def run_batch(lines, mode: str = "exact", ell=None, encoding: str = "ascii7",
+              budget: float = 4000.0, key_encoding: str = "negated", preprocess: bool = False,
+              ctx: Context | None = None, seed: int = 0):
+    """cli::run_batch (cli.cpp:164-210): one JSON object {"a":..,"b":..} per
+    line -> one report line (or {"error": ...}) per line, input order kept.
+    All valid lines of a non-preprocessed batch are traversed together: every
+    pair's same-index anti-diagonal shares one GPU launch."""
+    import json
+    from . import Error
+    ctx = ctx if ctx is not None else _context(seed, budget)
+    spec = AlphabetSpec.by_name(encoding)
+    out = [None] * len(lines)
+    todo = []
+    for idx, text in enumerate(lines):
+        try:
+            j = json.loads(text)
+        except Exception as e:
+            out[idx] = json.dumps({"error": f"bad JSON: {e}"}, separators=(",", ":"))
+            continue
+        if not (isinstance(j, dict) and isinstance(j.get("a"), str) and isinstance(j.get("b"), str)):
+            out[idx] = json.dumps({"error": 'each line needs string fields "a" and "b"'},
+                                  separators=(",", ":"))
+            continue
+        a, b = j["a"], j["b"]
+        try:
+            band = _resolve_band(mode, ell, len(a), len(b))
+            for s in (a, b):
+                for ch in s:
+                    spec.code_of(ch)
+            if not band.covers(len(a), len(b)):
+                raise BandTooNarrow(f"band half-width {band.half_width} below length difference")
+            if budget < 11.0:
+                raise InvalidParams("noise budget below 11: refreshed operands alone exceed it")
+        except Error as e:
+            out[idx] = json.dumps({"error": str(e)}, separators=(",", ":"))
+            continue
+        todo.append((idx, a, b, band))
+    if preprocess:
+        for idx, a, b, _ in todo:
+            try:
+                rep = compute(a, b, mode, ell, encoding, budget, key_encoding, True, ctx=ctx)
+                out[idx] = report_json(rep)
+            except Error as e:
+                out[idx] = json.dumps({"error": str(e)}, separators=(",", ":"))
+        return out
+    if todo:
+        enc = [(encrypt_string(a, spec, ctx), encrypt_string(b, spec, ctx)) for _, a, b, _ in todo]
+        runs = distance_batch(ctx, enc, [band for *_, band in todo], key_encoding)
+        dists = ctx.decrypt([r.score for r in runs])
+        for (idx, a, b, band), r, d in zip(todo, runs, dists):
+            rep = {"distance": int(d), "mode": mode, "half_width": band.half_width,
+                   "visited_cells": r.visited_cells,
+                   "pbs_total": r.equality_pbs + r.kernel_pbs + r.refreshes,
+                   "pbs_equality": r.equality_pbs, "pbs_kernel": r.kernel_pbs,
+                   "refresh_count": r.refreshes, "preprocessing_pbs": 0,
+                   "max_key_variance": r.max_key_variance}
+            out[idx] = report_json(rep)
+        ctx.release([r.score for r in runs])
+        for x, y in enc:
+            for t in (x.chars, y.chars):
+                if t.size:
+                    ctx.release(t)
+    return out
+
+
+# ------------------------------------------------------------ LEQT v2 container
+def _alphabet_meta(spec: AlphabetSpec) -> bytes:
+    """The v1 alphabet section (preprocess.cpp:144-152): name, widths, chars."""
+    import struct
+    name = spec.name.encode()
+    b = struct.pack("<I", len(name)) + name + struct.pack("<I", len(spec.widths))
+    b += b"".join(struct.pack("<i", w) for w in spec.widths)
+    chars = spec.charset()
+    b += struct.pack("<I", len(chars))
+    b += b"".join(bytes([ord(c)]) + struct.pack("<i", spec.code_of(c)) for c in chars)
+    return b
+
+
+def _parse_meta(meta: bytes) -> AlphabetSpec:
+    import struct
+    from . import FormatError
+    try:
+        p = 0
+        (ln,) = struct.unpack_from("<I", meta, p); p += 4
+        name = meta[p:p + ln].decode(); p += ln
+        (nw,) = struct.unpack_from("<I", meta, p); p += 4
+        widths = list(struct.unpack_from(f"<{nw}i", meta, p)); p += 4 * nw
+        (nc,) = struct.unpack_from("<I", meta, p); p += 4
+        mapping = []
+        for _ in range(nc):
+            ch = chr(meta[p]); (code,) = struct.unpack_from("<i", meta, p + 1); p += 5
+            mapping.append((ch, code))
+    except Exception as e:
+        raise FormatError(f"truncated alphabet section: {e}")
+    return AlphabetSpec(name, widths, mapping)
+
+
+def save_eq_table(table: EqTable, f) -> int:
+    """preprocess::save_eq_table (preprocess.cpp:140-164), v2 with real
+    ciphertexts; f is a path or a binary file object. Returns bytes written."""
+    meta = _alphabet_meta(table.spec)
+    need = ctypes.c_uint64()
+    _check(lib().lv_eq_table_serialize(table._ctx._h, table._h, meta, len(meta), None, 0,
+                                       ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(lib().lv_eq_table_serialize(table._ctx._h, table._h, meta, len(meta), buf, need.value,
+                                       ctypes.byref(need)))
+    data = buf.raw[:need.value]
+    if isinstance(f, (str, bytes)) or hasattr(f, "__fspath__"):
+        with open(f, "wb") as fh:
+            fh.write(data)
+    else:
+        f.write(data)
+    return len(data)
+
+
+def load_eq_table(ctx: Context, f) -> EqTable:
+    """preprocess::load_eq_table (preprocess.cpp:166-194) for v2 files."""
+    if isinstance(f, (str, bytes)) or hasattr(f, "__fspath__"):
+        with open(f, "rb") as fh:
+            data = fh.read()
+    else:
+        data = f.read()
+    h = ctypes.c_void_p()
+    ml = ctypes.c_uint64()
+    meta = ctypes.create_string_buffer(max(1, len(data)))
+    _check(lib().lv_eq_table_deserialize(ctx._h, data, len(data), ctypes.byref(h), meta, len(data),
+                                         ctypes.byref(ml)))
+    spec = _parse_meta(meta.raw[:ml.value])
+    import struct
+    p = 12 + ml.value + 20  # header, alphabet, n/N/k/seed (already validated)
+    length, nrows = struct.unpack_from("<QI", data, p)
+    p += 12
+    subset = []
+    for _ in range(nrows):  # row characters, skipping the ciphertext payloads
+        subset.append(chr(data[p]))
+        p += 1
+        for _ in range(length):
+            (terms,) = struct.unpack_from("<I", data, p)
+            p += 4 + 4 * terms + 8 * (ctx.N + 1)
+    return EqTable(ctx, h, spec, length, subset)

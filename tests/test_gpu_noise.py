@@ -32,7 +32,7 @@ def rotate(tp, e, N):
     out = np.zeros(N, np.uint64)
     for j in range(N):
         s = (j - e) % (2 * N)
-        out[j] = tp[s] if s < N else np.uint64(0) - tp[s - N]
+        out[j] = tp[s] if s < N else np.uint64((-int(tp[s - N])) % (1 << 64))
     return out
 
 
