@@ -81,6 +81,8 @@ def lib():
         L.orc_blind_rotate_batch.argtypes = [vp, ctypes.c_size_t, u32p, u64p, u64p, ctypes.c_int,
                                              ctypes.c_int]
         L.orc_pbs.argtypes = [vp, u64p, i32p, u64p, ctypes.c_int]
+        L.orc_fft_phase_error_var.restype = ctypes.c_double
+        L.orc_fft_phase_error_var.argtypes = [vp, u32p, u64p]
         L.orc_pbs_batch.argtypes = [vp, ctypes.c_size_t, u64p, i32p, u64p, ctypes.c_int, ctypes.c_int]
         L.orc_fft_forward_i64.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double)]
         L.orc_fft_backward_torus.argtypes = [vp, ctypes.POINTER(ctypes.c_double), u64p]
@@ -194,6 +196,13 @@ class Oracle:
         lib().orc_blind_rotate_batch(self._c, ms.shape[0], _p(ms, ctypes.c_uint32),
                                      _p(tp, ctypes.c_uint64), _p(out, ctypes.c_uint64), mode, threads)
         return out
+
+    def fft_phase_error_var(self, ms: np.ndarray, tp: np.ndarray) -> float:
+        """Phase variance the f64 FFT adds over one blind rotation (exact
+        products computed alongside on the same inputs)."""
+        ms = np.ascontiguousarray(ms, np.uint32)
+        tp = np.ascontiguousarray(tp, np.uint64)
+        return lib().orc_fft_phase_error_var(self._c, _p(ms, ctypes.c_uint32), _p(tp, ctypes.c_uint64))
 
     def sample_extract(self, glwe: np.ndarray) -> np.ndarray:
         glwe = np.ascontiguousarray(glwe, np.uint64)

@@ -46,6 +46,8 @@ struct orc_ctx {
   double* tw;      /* W[t] = exp(-2 pi i t / M), t < M/2, interleaved */
   double* twist;   /* zeta^j = exp(i pi j / N), j < M */
   double* untwist; /* zeta^-j / M */
+  double* tw_dd;   /* W[t], t < M/2, as (re.hi, re.lo, im.hi, im.lo) */
+  double* twist_dd; /* zeta^j, j < M, same packing */
   uint32_t M;      /* N/2 */
   uint32_t logM;
 };
@@ -293,6 +295,75 @@ static void backward_torus(const orc_ctx* c, double* spec /* destroyed */, uint6
   }
 }
 
+/* Key-preparation transform of the BSK (keygen only): the same DIF network
+ * in double-double arithmetic with double-double twist/twiddle tables,
+ * rounded to double once at the end. Removes the f64 FFT's own rounding of
+ * the BSK spectrum (a third of the external product's FFT error, DESIGN.md
+ * §2). Operation order is a specification shared with bsk_fourier_dd_kernel
+ * (csrc/kernels.cu). */
+typedef struct {
+  double hi, lo;
+} dd_t;
+typedef struct {
+  dd_t re, im;
+} cdd_t;
+
+static inline dd_t dd_two_sum(double a, double b) {
+  const double s = a + b;
+  const double bb = s - a;
+  const double e = (a - (s - bb)) + (b - bb);
+  return (dd_t){s, e};
+}
+static inline dd_t dd_fast(double a, double b) {
+  const double s = a + b;
+  return (dd_t){s, b - (s - a)};
+}
+static inline dd_t dd_add(dd_t x, dd_t y) {
+  const dd_t s = dd_two_sum(x.hi, y.hi);
+  return dd_fast(s.hi, s.lo + (x.lo + y.lo));
+}
+static inline dd_t dd_sub(dd_t x, dd_t y) {
+  const dd_t s = dd_two_sum(x.hi, -y.hi);
+  return dd_fast(s.hi, s.lo + (x.lo - y.lo));
+}
+static inline dd_t dd_mul(dd_t x, dd_t y) {
+  const double p = x.hi * y.hi;
+  double e = fma(x.hi, y.hi, -p);
+  e = fma(x.hi, y.lo, e);
+  e = fma(x.lo, y.hi, e);
+  return dd_fast(p, e);
+}
+static inline cdd_t cdd_mul(cdd_t a, cdd_t b) {
+  return (cdd_t){dd_sub(dd_mul(a.re, b.re), dd_mul(a.im, b.im)),
+                 dd_add(dd_mul(a.re, b.im), dd_mul(a.im, b.re))};
+}
+static inline dd_t dd_from_i64(int64_t a) {
+  const double hi = (double)(int64_t)((uint64_t)a & ~UINT64_C(0x7FF)); /* <= 53 bits: exact */
+  const double lo = (double)(int64_t)((uint64_t)a & UINT64_C(0x7FF));
+  return dd_two_sum(hi, lo);
+}
+static inline cdd_t cdd_load(const double* t) { return (cdd_t){{t[0], t[1]}, {t[2], t[3]}}; }
+
+static void forward_i64_dd(const orc_ctx* c, const int64_t* a, double* out, cdd_t* x) {
+  const uint32_t M = c->M;
+  for (uint32_t j = 0; j < M; ++j)
+    x[j] = cdd_mul((cdd_t){dd_from_i64(a[j]), dd_from_i64(a[j + M])}, cdd_load(c->twist_dd + 4 * j));
+  for (uint32_t s = 0; s < c->logM; ++s) {
+    const uint32_t half = M >> (s + 1);
+    for (uint32_t blk = 0; blk < M; blk += 2 * half)
+      for (uint32_t j = 0; j < half; ++j) {
+        const cdd_t u = x[blk + j], v = x[blk + j + half];
+        x[blk + j] = (cdd_t){dd_add(u.re, v.re), dd_add(u.im, v.im)};
+        x[blk + j + half] = cdd_mul((cdd_t){dd_sub(u.re, v.re), dd_sub(u.im, v.im)},
+                                    cdd_load(c->tw_dd + 4 * ((size_t)j << s)));
+      }
+  }
+  for (uint32_t f = 0; f < M; ++f) {
+    out[2 * f] = x[f].re.hi + x[f].re.lo;
+    out[2 * f + 1] = x[f].im.hi + x[f].im.lo;
+  }
+}
+
 void orc_fft_forward_i64(const orc_ctx* c, const int64_t* poly, double* spec) {
   forward_i64(c, poly, spec);
 }
@@ -345,6 +416,27 @@ static void build_tables(orc_ctx* c) {
   }
   free(fine);
   free(coarse);
+  /* double-double tables for the BSK transform: hi = rn(v), lo = rn(v - hi) */
+  c->tw_dd = (double*)malloc(sizeof(double) * 4 * (M / 2));
+  c->twist_dd = (double*)malloc(sizeof(double) * 4 * M);
+  for (uint32_t t = 0; t < M / 2; ++t) {
+    const long double ang = 2.0L * PI * (long double)t / (long double)M;
+    const long double cr = cosl(ang), ci = -sinl(ang);
+    double* e = c->tw_dd + 4 * t;
+    e[0] = (double)cr;
+    e[1] = (double)(cr - (long double)e[0]);
+    e[2] = (double)ci;
+    e[3] = (double)(ci - (long double)e[2]);
+  }
+  for (uint32_t j = 0; j < M; ++j) {
+    const long double ang = PI * (long double)j / (long double)N;
+    const long double cr = cosl(ang), ci = sinl(ang);
+    double* e = c->twist_dd + 4 * j;
+    e[0] = (double)cr;
+    e[1] = (double)(cr - (long double)e[0]);
+    e[2] = (double)ci;
+    e[3] = (double)(ci - (long double)e[2]);
+  }
 }
 
 /* ------------------------------------------------------------------ */
@@ -362,6 +454,7 @@ static void bsk_range(void* a, size_t lo, size_t hi) {
   const uint32_t N = p->N, k = p->k, rows = rows_of(p), L = p->pbs_level;
   double* spec = (double*)malloc(sizeof(double) * 2 * c->M);
   int64_t* tmp = (int64_t*)malloc(sizeof(int64_t) * N);
+  cdd_t* work = (cdd_t*)malloc(sizeof(cdd_t) * c->M);
   for (size_t i = lo; i < hi; ++i) {
     for (uint32_t r = 0; r < rows; ++r) {
       const uint32_t comp = r / L, lev = r % L + 1;
@@ -386,7 +479,7 @@ static void bsk_range(void* a, size_t lo, size_t hi) {
       for (uint32_t o = 0; o <= k; ++o) {
         const uint64_t* poly = row + (size_t)o * N;
         for (uint32_t cc = 0; cc < N; ++cc) tmp[cc] = (int64_t)poly[cc];
-        forward_i64(c, tmp, spec);
+        forward_i64_dd(c, tmp, spec, work);
         memcpy(c->bskf + (((size_t)i * rows + r) * (k + 1) + o) * 2 * c->M, spec,
                sizeof(double) * 2 * c->M);
       }
@@ -394,6 +487,7 @@ static void bsk_range(void* a, size_t lo, size_t hi) {
   }
   free(spec);
   free(tmp);
+  free(work);
 }
 
 static void ksk_range(void* a, size_t lo, size_t hi) {
@@ -445,6 +539,8 @@ void orc_destroy(orc_ctx* c) {
   free(c->tw);
   free(c->twist);
   free(c->untwist);
+  free(c->tw_dd);
+  free(c->twist_dd);
   free(c);
 }
 
@@ -625,6 +721,61 @@ void orc_blind_rotate(const orc_ctx* c, const uint32_t* ms, const uint64_t* tp,
   free(specs);
   free(facc);
   free(dig);
+}
+
+/* Noise accounting (test infrastructure): one FFT-mode blind rotation in
+ * which every external product is also computed exactly on the same input;
+ * returns the sum over CMUX steps of the mean squared phase of
+ * (FFT product - exact product), i.e. the variance the f64 FFT adds to the
+ * accumulator phase, free of the run-to-run spread of a noise estimate. */
+double orc_fft_phase_error_var(const orc_ctx* c, const uint32_t* ms, const uint64_t* tp) {
+  const orc_params* p = &c->p;
+  const uint32_t N = p->N, k = p->k, n = p->n, M = c->M;
+  const size_t glen = (size_t)(k + 1) * N;
+  uint64_t* acc = (uint64_t*)calloc(glen, sizeof(uint64_t));
+  poly_rotate(tp, acc + (size_t)k * N, N, (2 * N - ms[n]) % (2 * N));
+  uint64_t* diff = (uint64_t*)malloc(sizeof(uint64_t) * glen);
+  uint64_t* ext = (uint64_t*)malloc(sizeof(uint64_t) * glen);
+  uint64_t* ex2 = (uint64_t*)malloc(sizeof(uint64_t) * glen);
+  uint64_t* ph = (uint64_t*)malloc(sizeof(uint64_t) * N);
+  double* specs = (double*)malloc(sizeof(double) * 2 * M * rows_of(p));
+  double* facc = (double*)malloc(sizeof(double) * 2 * M);
+  int64_t* dig = (int64_t*)malloc(sizeof(int64_t) * N * p->pbs_level);
+  double total = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t a = ms[i];
+    if (a == 0) continue;
+    for (uint32_t comp = 0; comp <= k; ++comp) {
+      poly_rotate(acc + (size_t)comp * N, diff + (size_t)comp * N, N, a);
+      for (uint32_t j = 0; j < N; ++j) diff[(size_t)comp * N + j] -= acc[(size_t)comp * N + j];
+    }
+    external_product_fft(c, i, diff, ext, specs, facc, dig);
+    external_product_exact(c, i, diff, ex2, dig);
+    for (size_t j = 0; j < glen; ++j) ex2[j] = ext[j] - ex2[j];
+    /* phase = B - sum_q A_q * S_q */
+    memcpy(ph, ex2 + (size_t)k * N, sizeof(uint64_t) * N);
+    for (uint32_t q = 0; q < k; ++q) {
+      uint64_t* neg = diff; /* reuse as scratch: -A_q */
+      for (uint32_t j = 0; j < N; ++j) neg[j] = (uint64_t)0 - ex2[(size_t)q * N + j];
+      poly_mul_binary_acc(ph, neg, c->sk_glwe + (size_t)q * N, N);
+    }
+    double s = 0;
+    for (uint32_t j = 0; j < N; ++j) {
+      const double e = (double)(int64_t)ph[j];
+      s += e * e;
+    }
+    total += s / N;
+    for (size_t j = 0; j < glen; ++j) acc[j] += ext[j];
+  }
+  free(acc);
+  free(diff);
+  free(ext);
+  free(ex2);
+  free(ph);
+  free(specs);
+  free(facc);
+  free(dig);
+  return total;
 }
 
 void orc_sample_extract(const orc_ctx* c, const uint64_t* glwe, uint64_t* out) {

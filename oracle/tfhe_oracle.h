@@ -91,6 +91,9 @@ void orc_sample_extract(const orc_ctx* c, const uint64_t* glwe, uint64_t* out_bi
 /* count blind rotations (ms rows of n+1, one test polynomial) over threads. */
 void orc_blind_rotate_batch(const orc_ctx* c, size_t count, const uint32_t* ms,
                             const uint64_t* tp, uint64_t* glwe_out, int mode, int threads);
+/* Sum over CMUX steps of the mean squared phase of (FFT - exact) external
+ * product on the same input: the variance the f64 FFT adds (noise tests). */
+double orc_fft_phase_error_var(const orc_ctx* c, const uint32_t* ms, const uint64_t* tp);
 
 /* Whole PBS: KS -> MS -> BR -> SE. */
 void orc_pbs(const orc_ctx* c, const uint64_t* in_big, const int32_t lut[16],

@@ -385,10 +385,36 @@ static void keygen(lv_ctx* c) {
                                                       c->d_sk_glwe, d_bsk);
   LV_CUDA(cudaGetLastError());
   LV_CUDA(cudaMalloc(&c->d_bskf, (size_t)n * 32 * 128 * sizeof(double2)));
-  bsk_fourier_kernel<<<n * kRows, 128, 0, c->stream>>>(d_bsk, c->d_tw, c->d_twist, c->d_bskf);
+  // double-double twiddle / twist tables for the BSK transform (oracle
+  // build_tables: hi = rn(v), lo = rn(v - hi) from long double)
+  std::vector<double4> tw_dd(kM / 2), twist_dd(kM);
+  {
+    const long double PI = 3.141592653589793238462643383279502884L;
+    auto split = [](long double cr, long double ci) {
+      const double rh = (double)cr, ih = (double)ci;
+      return make_double4(rh, (double)(cr - (long double)rh), ih, (double)(ci - (long double)ih));
+    };
+    for (uint32_t t = 0; t < kM / 2; ++t) {
+      const long double ang = 2.0L * PI * (long double)t / (long double)kM;
+      tw_dd[t] = split(cosl(ang), -sinl(ang));
+    }
+    for (uint32_t j = 0; j < kM; ++j) {
+      const long double ang = PI * (long double)j / (long double)kN;
+      twist_dd[j] = split(cosl(ang), sinl(ang));
+    }
+  }
+  double4 *d_tw_dd = nullptr, *d_twist_dd = nullptr;
+  LV_CUDA(cudaMalloc(&d_tw_dd, tw_dd.size() * sizeof(double4)));
+  LV_CUDA(cudaMalloc(&d_twist_dd, twist_dd.size() * sizeof(double4)));
+  LV_CUDA(cudaMemcpy(d_tw_dd, tw_dd.data(), tw_dd.size() * sizeof(double4), cudaMemcpyHostToDevice));
+  LV_CUDA(cudaMemcpy(d_twist_dd, twist_dd.data(), twist_dd.size() * sizeof(double4),
+                     cudaMemcpyHostToDevice));
+  bsk_fourier_kernel<<<n * kRows * 2, 512, 0, c->stream>>>(d_bsk, d_tw_dd, d_twist_dd, c->d_bskf);
   LV_CUDA(cudaGetLastError());
   LV_CUDA(cudaStreamSynchronize(c->stream));
   LV_CUDA(cudaFree(d_bsk));
+  LV_CUDA(cudaFree(d_tw_dd));
+  LV_CUDA(cudaFree(d_twist_dd));
 }
 
 std::array<int32_t, 16> eq_lut_entries(int scale) {  // equality.cpp:31-36

@@ -484,37 +484,84 @@ __global__ void keygen_bsk_kernel(uint64_t seed, uint32_t noise_log2, const uint
   }
 }
 
-// Fourier BSK: one CTA (128 threads) per GGSW row (i, r), both output
-// components transformed in lockstep with the same fft_forward the blind
-// rotation uses, then stored in the MAC layout [i][q*4 + r*2 + o][t].
-__global__ void __launch_bounds__(128)
-bsk_fourier_kernel(const uint64_t* bsk, const double2* __restrict__ tw,
-                   const double2* __restrict__ twist, double2* bskf) {
-  __shared__ double2 buf[2 * kM];
+// Fourier BSK (key preparation, once per context): the same DIF network as
+// the blind rotation's transform, but in double-double arithmetic with
+// double-double twist/twiddle tables, rounded to double once at the end.
+// The BSK spectrum then carries one rounding instead of the f64 FFT's
+// accumulated error — a third of the external product's FFT error
+// (DESIGN.md §2). Operation order = oracle forward_i64_dd (bit-exact).
+// One CTA of 512 threads per polynomial (i, r, o), 32 KB of shared memory;
+// output in the MAC layout [i][q*4 + r*2 + o][t] for bin f = 8t + q,
+// pre-scaled by 2^-10 (exact).
+struct dd_t {
+  double hi, lo;
+};
+struct cdd_t {
+  dd_t re, im;
+};
+__device__ __forceinline__ dd_t dd_two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  const double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+  return {s, e};
+}
+__device__ __forceinline__ dd_t dd_fast(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ dd_t dd_add(dd_t x, dd_t y) {
+  const dd_t s = dd_two_sum(x.hi, y.hi);
+  return dd_fast(s.hi, __dadd_rn(s.lo, __dadd_rn(x.lo, y.lo)));
+}
+__device__ __forceinline__ dd_t dd_sub(dd_t x, dd_t y) {
+  const dd_t s = dd_two_sum(x.hi, -y.hi);
+  return dd_fast(s.hi, __dadd_rn(s.lo, __dsub_rn(x.lo, y.lo)));
+}
+__device__ __forceinline__ dd_t dd_mul(dd_t x, dd_t y) {
+  const double p = __dmul_rn(x.hi, y.hi);
+  double e = __fma_rn(x.hi, y.hi, -p);
+  e = __fma_rn(x.hi, y.lo, e);
+  e = __fma_rn(x.lo, y.hi, e);
+  return dd_fast(p, e);
+}
+__device__ __forceinline__ cdd_t cdd_mul(cdd_t a, cdd_t b) {
+  return {dd_sub(dd_mul(a.re, b.re), dd_mul(a.im, b.im)),
+          dd_add(dd_mul(a.re, b.im), dd_mul(a.im, b.re))};
+}
+__device__ __forceinline__ dd_t dd_from_i64(uint64_t a) {
+  const double hi = (double)(int64_t)(a & ~0x7FFull);  // <= 53 significant bits: exact
+  const double lo = (double)(int64_t)(a & 0x7FFull);
+  return dd_two_sum(hi, lo);
+}
+__device__ __forceinline__ cdd_t cdd_load(const double4* t, uint32_t k) {
+  const double4 v = t[k];
+  return {{v.x, v.y}, {v.z, v.w}};
+}
+
+__global__ void __launch_bounds__(512)
+bsk_fourier_kernel(const uint64_t* bsk, const double4* __restrict__ tw_dd,
+                   const double4* __restrict__ twist_dd, double2* bskf) {
+  __shared__ cdd_t x[kM];
   const uint32_t t = threadIdx.x;
-  const uint32_t i = blockIdx.x / kRows, r = blockIdx.x % kRows;
-  const uint64_t rowi = (uint64_t)i * kRows + r;
-  double2 X[2][8];
-#pragma unroll
-  for (int o = 0; o < 2; ++o) {
-    const uint64_t* poly = bsk + (rowi * (kK + 1) + o) * kN;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint32_t x = t + 128 * q;
-      const double re = (double)(int64_t)poly[x];
-      const double im = (double)(int64_t)poly[x + kM];
-      X[o][q] = cmul(make_double2(re, im), twist_at(twist, x));
-    }
+  const uint32_t o = blockIdx.x & 1, rowi = blockIdx.x >> 1;  // rowi = i * kRows + r
+  const uint32_t i = rowi / kRows, r = rowi % kRows;
+  const uint64_t* poly = bsk + ((uint64_t)rowi * (kK + 1) + o) * kN;
+  for (uint32_t j = t; j < kM; j += blockDim.x)
+    x[j] = cdd_mul({dd_from_i64(poly[j]), dd_from_i64(poly[j + kM])}, cdd_load(twist_dd, j));
+  __syncthreads();
+  for (uint32_t s = 0; s < kLogM; ++s) {
+    const uint32_t half = kM >> (s + 1);
+    const uint32_t j = t & (half - 1), blk = (t >> (kLogM - 1 - s)) * 2 * half;
+    const cdd_t u = x[blk + j], v = x[blk + j + half];
+    x[blk + j] = {dd_add(u.re, v.re), dd_add(u.im, v.im)};
+    x[blk + j + half] = cdd_mul({dd_sub(u.re, v.re), dd_sub(u.im, v.im)}, cdd_load(tw_dd, j << s));
+    __syncthreads();
   }
-  fft_forward<2>(X, buf, tw, t);
-#pragma unroll
-  for (int q = 0; q < 8; ++q)
-#pragma unroll
-    for (int o = 0; o < 2; ++o)
-      // stored pre-scaled by 1/M = 2^-10 (exact): the untwist then needs no
-      // scaling multiply and every rounding downstream is unchanged
-      bskf[(size_t)i * (32 * 128) + (q * 4 + r * 2 + o) * 128 + t] =
-          make_double2(__dmul_rn(X[o][q].x, 0x1p-10), __dmul_rn(X[o][q].y, 0x1p-10));
+  for (uint32_t f = t; f < kM; f += blockDim.x) {
+    const double re = __dadd_rn(x[f].re.hi, x[f].re.lo), im = __dadd_rn(x[f].im.hi, x[f].im.lo);
+    bskf[(size_t)i * (32 * 128) + ((f & 7) * 4 + r * 2 + o) * 128 + (f >> 3)] =
+        make_double2(__dmul_rn(re, 0x1p-10), __dmul_rn(im, 0x1p-10));
+  }
 }
 
 // Debug / parity entry: forward transform of one integer polynomial, output

@@ -111,8 +111,8 @@ __global__ void keygen_ksk_kernel(uint64_t seed, uint32_t n, uint32_t noise_log2
                                   const uint8_t* sk_small, const uint8_t* sk_glwe, uint64_t* ksk);
 __global__ void keygen_bsk_kernel(uint64_t seed, uint32_t noise_log2, const uint8_t* sk_small,
                                   const uint8_t* sk_glwe, uint64_t* bsk);
-__global__ void bsk_fourier_kernel(const uint64_t* bsk, const double2* tw, const double2* twist,
-                                   double2* bskf);
+__global__ void bsk_fourier_kernel(const uint64_t* bsk, const double4* tw_dd,
+                                   const double4* twist_dd, double2* bskf);
 __global__ void fft_forward_debug_kernel(const int64_t* poly, const double2* tw,
                                          const double2* twist, double2* spec);
 __global__ void fft_backward_debug_kernel(const double2* spec, const double2* tw,
