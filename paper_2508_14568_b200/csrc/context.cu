@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -175,6 +176,18 @@ static void launch_keyswitch(lv_ctx* c, const LinDesc* d_desc, uint32_t count, u
   LV_CUDA(cudaGetLastError());
 }
 
+// Waves of at most br_pair_max items (default: half the SMs) leave SMs idle
+// in the single-CTA form; they run the CTA-pair form instead, two SMs per
+// item.
+void launch_blind_rotate(lv_ctx* c, const BrArgs& ba, uint32_t count) {
+  if (!count) return;
+  if (count <= c->br_pair_max)
+    blind_rotate_pair_kernel<<<2 * count, 128, blind_rotate_pair_smem_bytes(c->p.n), c->stream>>>(ba);
+  else
+    blind_rotate_kernel<<<count, 128, blind_rotate_smem_bytes(c->p.n), c->stream>>>(ba);
+  LV_CUDA(cudaGetLastError());
+}
+
 void launch_pbs_dev(lv_ctx* c, const LinDesc* d_desc, const uint32_t* d_lut, const BrOut* d_out,
                     uint32_t count, cudaEvent_t ks_done) {
   if (!count) return;
@@ -184,8 +197,7 @@ void launch_pbs_dev(lv_ctx* c, const LinDesc* d_desc, const uint32_t* d_lut, con
   if (ks_done) LV_CUDA(cudaEventRecord(ks_done, c->stream));
   BrArgs ba{d_ms, stride, d_lut, c->d_tp, c->d_bskf, c->d_tw, c->d_twist, c->p.n,
             c->d_pool, kBigStride, d_out};
-  blind_rotate_kernel<<<count, 128, blind_rotate_smem_bytes(c->p.n), c->stream>>>(ba);
-  LV_CUDA(cudaGetLastError());
+  launch_blind_rotate(c, ba, count);
 }
 
 void run_pbs_items(lv_ctx* c, const std::vector<PbsItem>& items) {
@@ -493,6 +505,16 @@ int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
                                    (int)blind_rotate_smem_bytes(p.n)));
       LV_CUDA(cudaFuncSetAttribute(ks_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)ks_tc_smem_bytes()));
+      LV_CUDA(cudaFuncSetAttribute(blind_rotate_pair_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)blind_rotate_pair_smem_bytes(p.n)));
+      {
+        int sms = 148;
+        LV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+        c->br_pair_max = (uint32_t)sms / 2;
+        if (const char* e = std::getenv("LVB_BR_PAIR_MAX"))
+          c->br_pair_max = (uint32_t)std::strtoul(e, nullptr, 10);
+      }
       build_tables(c);
       keygen(c);
       c->min_lut[0] = lut_id(c, min_lut_entries(false));
@@ -839,8 +861,7 @@ int lv_debug_blind_rotate(lv_ctx* c, const uint32_t* ms, const uint32_t* luts, s
       LV_CUDA(cudaMalloc(&dglwe, count * 2 * kN * sizeof(uint64_t)));
       ba.glwe_out = dglwe;
     }
-    blind_rotate_kernel<<<(uint32_t)count, 128, blind_rotate_smem_bytes(c->p.n), c->stream>>>(ba);
-    LV_CUDA(cudaGetLastError());
+    launch_blind_rotate(c, ba, (uint32_t)count);
     download_rows(c, s, out);
     if (dglwe)
       LV_CUDA(cudaMemcpyAsync(glwe_out, dglwe, count * 2 * kN * 8, cudaMemcpyDeviceToHost, c->stream));

@@ -110,6 +110,7 @@ struct lv_ctx {
 
   std::map<std::string, lvb::PairPlan> plan_cache;
   uint32_t min_lut[2] = {0, 0};
+  uint32_t br_pair_max = 0;  // waves up to this size run blind_rotate_pair_kernel
   uint32_t identity_lut = 0;
 };
 

@@ -7,6 +7,7 @@
 // Replaces SimBackend::pbs (proj/src/backend.cpp:61-70), whose whole effect
 // is negacyclic_eval(lut, x) (proj/src/lut.cpp:9-16) on a plaintext; here
 // the same table is applied homomorphically to real LWE ciphertexts.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -245,6 +246,168 @@ blind_rotate_kernel(BrArgs a) {
 size_t blind_rotate_smem_bytes(uint32_t n) {
   return 2 * kN * 8 + kXchgBufs * kM * 16 + ((n + 1) * 2 + 15) / 16 * 16;
 }
+
+// ------------------------------------------------------- BR, CTA pair
+// Latency form of the blind rotation for waves too small to fill the GPU:
+// a cluster of 2 CTAs per item on 2 SMs (the launch requests more than half
+// an SM's shared memory so the pair cannot share one SM), CTA p owning GLWE
+// polynomial p (0 = mask, 1 = body). Per CMUX each CTA decomposes and
+// transforms its own polynomial, publishes the spectrum in its shared
+// memory, and after a cluster barrier reads the partner's spectrum through
+// distributed shared memory to form its own output o = p:
+// D0 * BSK[0][o] + D1 * BSK[1][o] (the single-CTA kernel's FMA order, so
+// results are bit-identical), then inverse-transforms and accumulates it.
+namespace cg = cooperative_groups;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+blind_rotate_pair_kernel(BrArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* acc = reinterpret_cast<uint64_t*>(smem);                    // [kN] own polynomial
+  double2* buf = reinterpret_cast<double2*>(smem + kN * 8);             // [kM] FFT exchanges
+  double2* spec = reinterpret_cast<double2*>(smem + kN * 8 + kM * 16);  // [2][8][128] published
+  uint16_t* ms = reinterpret_cast<uint16_t*>(smem + kN * 8 + 3 * kM * 16);
+  cg::cluster_group cluster = cg::this_cluster();
+  const uint32_t p = cluster.block_rank();
+  const double2* pspec = cluster.map_shared_rank(spec, p ^ 1u);
+  const uint32_t t = threadIdx.x;
+  const uint32_t item = blockIdx.x >> 1;
+  const uint32_t n = a.n;
+
+  const uint16_t* ms_g = a.ms + (size_t)item * a.ms_stride;
+  for (uint32_t i = t; i <= n; i += 128) ms[i] = ms_g[i];
+  __syncthreads();
+  {
+    // ACC = X^{-b~} * (0, TP): the mask starts at 0, the body at the rotated TP
+    const uint64_t* tp = a.test_polys + (size_t)a.lut_of_item[item] * kN;
+    const uint32_t e = (2 * kN - ms[n]) % (2 * kN);
+    for (uint32_t j = t; j < kN; j += 128) {
+      const uint32_t s = (j + 2 * kN - e) % (2 * kN);
+      acc[j] = p == 0 ? 0 : (s < kN ? tp[s] : (uint64_t)0 - tp[s - kN]);
+    }
+  }
+  const double2* __restrict__ tw = a.twiddles;
+  const double2 tw_fine = __ldg(a.twist + t);
+  double2 tz[8];  // twist of x = t + 128 r (fine[t] * coarse[r]), kept in registers
+#pragma unroll
+  for (int r = 0; r < 8; ++r) tz[r] = r == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]);
+  const double2* bsk_base = a.bskf + t;
+  uint64_t own[16];  // coefficients t + 128 r (+ kM) of the own polynomial
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    own[2 * r] = acc[t + 128 * r];
+    own[2 * r + 1] = acc[t + 128 * r + kM];
+  }
+  cluster.sync();  // the partner's shared memory is live before any DSMEM access
+
+  // The published spectrum alternates between two buffers by executed-CMUX
+  // parity, so the one cluster barrier per CMUX (after publishing) also
+  // guarantees the partner finished reading the buffer being overwritten
+  // (it read it two CMUXes ago, before arriving at the last barrier).
+  uint32_t parity = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    __syncthreads();  // previous update of acc visible to the rotated reads
+    const uint32_t rot = ms[i];
+    if (rot == 0) continue;  // uniform across the pair: both skip
+
+    // this CMUX's BSK row (bins 8t + q, outputs p), in flight during the forward FFT
+    double2 b0[8], b1[8];
+    {
+      const double2* bsk = bsk_base + (size_t)i * (32 * 128);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        b0[q] = ld_stream(bsk + (q * 4 + 0 + p) * 128);  // row 0, output p
+        b1[q] = ld_stream(bsk + (q * 4 + 2 + p) * 128);  // row 1, output p
+      }
+    }
+    double2 X[1][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const uint32_t x = t + 128 * r;
+      int32_t d[2];
+#pragma unroll
+      for (int hpart = 0; hpart < 2; ++hpart) {
+        const uint32_t j = x + hpart * kM;
+        const uint32_t s = (j + 2 * kN - rot) & (2 * kN - 1);
+        const uint64_t pv = acc[s & (kN - 1)];
+        const uint64_t rv = s < kN ? pv : (uint64_t)0 - pv;
+        d[hpart] = (int32_t)decomp1(rv - own[2 * r + hpart], kPbsBaseLog);
+      }
+      X[0][r] = cmul(make_double2((double)d[0], (double)d[1]), tz[r]);
+    }
+    fft_forward<1>(X, buf, tw, t);
+    double2* mine = spec + parity * kM;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) mine[q * 128 + t] = X[0][q];
+    cluster.sync();  // both spectra published
+    {
+      const double2* other_spec = pspec + parity * kM;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double2 other = other_spec[q * 128 + t];
+        const double2 d0 = p == 0 ? X[0][q] : other, d1 = p == 0 ? other : X[0][q];
+        double2 o;
+        o.x = __fma_rn(d0.x, b0[q].x, 0.0);
+        o.x = __fma_rn(-d0.y, b0[q].y, o.x);
+        o.y = __fma_rn(d0.x, b0[q].y, 0.0);
+        o.y = __fma_rn(d0.y, b0[q].x, o.y);
+        o.x = __fma_rn(d1.x, b1[q].x, o.x);
+        o.x = __fma_rn(-d1.y, b1[q].y, o.x);
+        o.y = __fma_rn(d1.x, b1[q].y, o.y);
+        o.y = __fma_rn(d1.y, b1[q].x, o.y);
+        X[0][q] = o;
+      }
+    }
+    parity ^= 1u;
+    __syncthreads();  // forward's last buffer reads precede the inverse's writes
+    fft_inverse_a<1>(X, buf, tw, t);  // its barriers also order the rotated reads before the update
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const double2 ut = make_double2(tz[r].x, -tz[r].y);
+      const uint32_t x = t + 128 * r;
+      const double2 z = cmul(X[0][r], ut);
+      own[2 * r] += f64_to_torus(z.x);
+      own[2 * r + 1] += f64_to_torus(z.y);
+      acc[x] = own[2 * r];
+      acc[x + kM] = own[2 * r + 1];
+    }
+  }
+  cluster.sync();  // no DSMEM reads of this CTA's buffers remain when it exits
+  __syncthreads();
+
+  if (a.glwe_out)
+    for (uint32_t j = t; j < kN; j += 128) a.glwe_out[(size_t)item * 2 * kN + p * kN + j] = acc[j];
+
+  // sample extract: the mask CTA writes a' (j < kN), the body CTA b' (j = kN)
+  const BrOut o = a.outs[item];
+  const uint32_t S = a.pool_stride;
+  const uint32_t j0 = p == 0 ? t : kN + t, j1 = p == 0 ? kN : kN + 1;
+  if (o.mode == 0) {
+    uint64_t* out = a.pool + (size_t)o.slot_a * S;
+    for (uint32_t j = j0; j < j1; j += 128)
+      out[j] = j == 0 ? acc[0]
+                      : (j == kN ? acc[0] + (uint64_t)(int64_t)o.body_add * kDelta
+                                 : (uint64_t)0 - acc[kN - j]);
+  } else {
+    uint64_t* dv = a.pool + (size_t)o.slot_a * S;
+    uint64_t* dh = a.pool + (size_t)o.slot_b * S;
+    uint64_t* sdv = o.snap_dv == kNoSlot ? nullptr : a.pool + (size_t)o.snap_dv * S;
+    uint64_t* sdh = o.snap_dh == kNoSlot ? nullptr : a.pool + (size_t)o.snap_dh * S;
+    for (uint32_t j = j0; j < j1; j += 128) {
+      const uint64_t step = j == 0 ? acc[0] : (j == kN ? acc[0] : (uint64_t)0 - acc[kN - j]);
+      const uint64_t v_in = dv[j], h_in = dh[j];
+      const uint64_t v_out = step - h_in, h_out = step - v_in;
+      dv[j] = v_out;
+      dh[j] = h_out;
+      if (sdv) sdv[j] = v_out;
+      if (sdh) sdh[j] = h_out;
+    }
+  }
+}
+
+// More than half of the SM's 228 KB, so the two CTAs of a pair (and pairs of
+// different items) never share an SM.
+size_t blind_rotate_pair_smem_bytes(uint32_t) { return 120 * 1024; }
 
 // ------------------------------------------------------------------ KS
 // Key switch (big key kN -> small key n) fused with the linear prologue

@@ -101,6 +101,8 @@ struct PhaseArgs {
 
 __global__ void blind_rotate_kernel(BrArgs a);
 size_t blind_rotate_smem_bytes(uint32_t n);
+__global__ void blind_rotate_pair_kernel(BrArgs a);
+size_t blind_rotate_pair_smem_bytes(uint32_t n);
 __global__ void keyswitch_kernel(KsArgs a);
 __global__ void linear_kernel(LinArgs a);
 __global__ void encrypt_kernel(EncArgs a);

@@ -132,3 +132,25 @@ def test_random_linear_circuits(ctx):
                 k = int(rng.integers(0, 32))
                 cts.append(ctx.scalar_add([cts[i]], k)[0]); plain.append((plain[i] + k) % 32)
         assert list(ctx.decrypt(cts)) == [int(p) for p in plain]
+
+
+@pytest.mark.parametrize("pair_max", [0, 1 << 30])
+def test_blind_rotate_variants_bit_exact(orc, pair_max, monkeypatch):
+    """Single-CTA (pair_max 0) and CTA-pair (cluster of 2 SMs, DSMEM
+    spectrum exchange) blind rotations both equal the FFT-spec oracle bit
+    for bit, including the whole GLWE accumulator."""
+    monkeypatch.setenv("LVB_BR_PAIR_MAX", str(pair_max))
+    c = L.Context(seed=0)
+    try:
+        lut = np.array(L.eq_lut(9), np.int32)
+        lid = c.lut(lut)
+        tp = orc.test_poly(lut)
+        rows = [orc.encrypt(v, 9100 + v) for v in (0, 3, 7, 12, 15)]
+        ms = np.stack([orc.modswitch(orc.keyswitch(r)) for r in rows])
+        out, glwe = c.debug_blind_rotate(ms, [lid] * len(rows), glwe=True)
+        want = orc.blind_rotate_batch(ms, tp, mode=0)
+        assert np.array_equal(glwe, want)
+        for i in range(len(rows)):
+            assert np.array_equal(out[i], orc.sample_extract(want[i]))
+    finally:
+        c.close()
