@@ -41,14 +41,8 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
 // then sample-extracts coefficient 0 into a big-key LWE.
 //
 // Shared memory: acc[2][N] u64 (32 KB) + FFT exchange buffer kXchgBufs x kM
-// double2 (16 KB split / 32 KB) + ms[n+1] u16.
-#ifndef LVB_OWN_ACC
-#define LVB_OWN_ACC 2
-#endif
-#ifndef LVB_BR_MIN_BLOCKS
-#define LVB_BR_MIN_BLOCKS (LVB_OWN_ACC ? 3 : 4)
-#endif
-__global__ void __launch_bounds__(128, LVB_BR_MIN_BLOCKS)
+// double2 (16 KB split / 32 KB) + ms[n+1] u16. 168 registers, 3 CTAs/SM.
+__global__ void __launch_bounds__(128, 3)
 blind_rotate_kernel(BrArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* acc = reinterpret_cast<uint64_t*>(smem);                   // [2][kN]
@@ -72,15 +66,13 @@ blind_rotate_kernel(BrArgs a) {
       acc[kN + j] = s < kN ? tp[s] : (uint64_t)0 - tp[s - kN];
     }
   }
-
   const double2* __restrict__ tw = a.twiddles;
-  const double2* __restrict__ twist = a.twist;
-
-#if LVB_OWN_ACC
-  // Thread t owns accumulator coefficients t + 128 r (+ 1024) of both
-  // polynomials: the forward FFT reads them there and fft_inverse_a writes
-  // the external product there, so they live in registers across the
-  // top-of-loop barrier; shared memory only serves the rotated reads.
+  // Thread t owns accumulator coefficients x = t + 128 r (and x + kM) of both
+  // polynomials: the forward FFT reads them in that layout and
+  // fft_inverse_a returns the external product in it, so each thread
+  // updates exactly the coefficients it decomposed; shared memory serves
+  // the rotated reads of the other threads.
+  const double2 tw_fine = __ldg(a.twist + t);  // twist of x = t + 128 r is fine[t] * coarse[r]
   __syncthreads();
   uint64_t own[2][16];  // [poly][2 r + half]
 #pragma unroll
@@ -90,8 +82,6 @@ blind_rotate_kernel(BrArgs a) {
       own[p][2 * r] = acc[p * kN + t + 128 * r];
       own[p][2 * r + 1] = acc[p * kN + t + 128 * r + kM];
     }
-  const double2 tw_fine = __ldg(twist + t);  // twist of x = t + 128 r is fine[t] * coarse[r]
-#endif
 
   for (uint32_t i = 0; i < n; ++i) {
     __syncthreads();
@@ -105,26 +95,17 @@ blind_rotate_kernel(BrArgs a) {
       const uint64_t* P = acc + p * kN;
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        const uint32_t x = t + 128 * r;
         int32_t d[2];  // |digit| <= 2^22: int32 -> f64 conversion is exact
 #pragma unroll
         for (int hpart = 0; hpart < 2; ++hpart) {
-          const uint32_t j = x + hpart * kM;
+          const uint32_t j = t + 128 * r + hpart * kM;
           const uint32_t s = (j + 2 * kN - rot) & (2 * kN - 1);
           const uint64_t pv = P[s & (kN - 1)];  // one load; the wrap only flips the sign
           const uint64_t rv = s < kN ? pv : (uint64_t)0 - pv;
-#if LVB_OWN_ACC
           d[hpart] = (int32_t)decomp1(rv - own[p][2 * r + hpart], kPbsBaseLog);
-#else
-          d[hpart] = (int32_t)decomp1(rv - P[j], kPbsBaseLog);
-#endif
         }
-#if LVB_OWN_ACC
         const double2 tz = r == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]);
         X[p][r] = cmul(make_double2((double)d[0], (double)d[1]), tz);
-#else
-        X[p][r] = cmul(make_double2((double)d[0], (double)d[1]), twist_at(twist, x));
-#endif
       }
     }
 
@@ -162,54 +143,25 @@ blind_rotate_kernel(BrArgs a) {
       }
     }
     __syncthreads();  // forward's last buffer reads precede the inverse's writes
-#if LVB_OWN_ACC
     fft_inverse_a<2>(X, buf, tw, t);
-    // untwist (conj(twist) / M, exact scaling), back to the torus, accumulate
-    // into the owned coefficients and publish them for the next rotation
+    // untwist (conj(twist); the 1/M is pre-applied to the BSK), back to the
+    // torus, accumulate into the owned coefficients and publish them
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const double2 tv = r == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]);
-      const double2 ut = make_double2(tv.x, -tv.y);  // the 1/M is pre-applied to the BSK
+      const double2 ut = make_double2(tv.x, -tv.y);
       const uint32_t x = t + 128 * r;
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
         const double2 z = cmul(X[p][r], ut);
-#if LVB_OWN_ACC == 2
         // re-read (unchanged during the CMUX) instead of holding 64 registers
-        // across the FFTs; owned only from here to the next rotation
-        own[p][2 * r] = acc[p * kN + x];
-        own[p][2 * r + 1] = acc[p * kN + x + kM];
-#endif
-        own[p][2 * r] += f64_to_torus(z.x);
-        own[p][2 * r + 1] += f64_to_torus(z.y);
+        // across the FFTs
+        own[p][2 * r] = acc[p * kN + x] + f64_to_torus(z.x);
+        own[p][2 * r + 1] = acc[p * kN + x + kM] + f64_to_torus(z.y);
         acc[p * kN + x] = own[p][2 * r];
         acc[p * kN + x + kM] = own[p][2 * r + 1];
       }
     }
-#else
-    fft_inverse<2>(X, buf, tw, t);
-
-    // untwist, back to the torus, accumulate
-    {
-      const uint32_t h = (t >> 4) & 1, u = 16 * (t >> 5) + (t & 15);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-#pragma unroll
-        for (int hi = 0; hi < 2; ++hi) {
-          const uint32_t x = u + 64 * (4 * h + q) + 512 * hi;
-          // untwist = conj(twist) / M (exact power-of-two scaling)
-          const double2 tv = twist_at(twist, x);
-          const double2 ut = make_double2(tv.x, -tv.y);  // the 1/M is pre-applied to the BSK
-#pragma unroll
-          for (int p = 0; p < 2; ++p) {
-            const double2 z = cmul(X[p][4 * hi + q], ut);
-            acc[p * kN + x] += f64_to_torus(z.x);
-            acc[p * kN + x + kM] += f64_to_torus(z.y);
-          }
-        }
-      }
-    }
-#endif
   }
   __syncthreads();
 
