@@ -313,7 +313,7 @@ def main():
         "gpu_launches": 3 * args.steps,  # per step: ks_digits, ks_mma (tcgen05), blind_rotate
         "clocks": clocks,
     }
-    if rank == 0 and not args.no_extras:
+    if rank == 0 and ws == 1 and not args.no_extras:  # extras and CPU baseline at N=1 only
         try:
             line["dp_cells"] = dp_cells(ctx, args.cfg5)
         except Exception as e:  # reported, never silently dropped
