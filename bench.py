@@ -212,6 +212,34 @@ def dp_cells(ctx, full_cfg5: bool = False):
         out[name] = {"cells": r["visited_cells"], "pbs": r["pbs_total"], "seconds": dt,
                      "cells_per_s": r["visited_cells"] / dt, "pbs_per_s": r["pbs_total"] / dt,
                      "distance": r["distance"], "waves": r["waves"]}
+    # database scan: cfg4's encrypted query, one equality table built once,
+    # against 64 plaintext server strings (cfg4's b and 63 more mutations)
+    a, b = W.cfg4()
+    spec = L.AlphabetSpec.dna4()
+    plains = [b] + [W.mutate(a, 6, W.MT19937(1000 + s), draw=W.dna) for s in range(63)]
+    xs = L.encrypt_string(a, spec, ctx)
+    t0 = time.perf_counter()
+    table, build_pbs = L.build_eq_table(ctx, xs, spec)
+    t1 = time.perf_counter()
+    bands = [L.BandSpec.exact(len(a), len(p)) for p in plains]
+    L.distance_preprocessed_batch(ctx, table, plains[:2], bands[:2])  # warm
+    t2 = time.perf_counter()
+    runs = L.distance_preprocessed_batch(ctx, table, plains, bands)
+    dists = ctx.decrypt([r.score for r in runs])
+    t3 = time.perf_counter()
+    cells = sum(r.visited_cells for r in runs)
+    out["cfg4_scan64"] = {"strings": len(plains), "cells": cells, "table_pbs": build_pbs,
+                          "table_seconds": t1 - t0, "scan_seconds": t3 - t2,
+                          "cells_per_s": cells / (t3 - t2),
+                          "pbs_per_s": sum(r.kernel_pbs for r in runs) / (t3 - t2),
+                          "distances_ok": all(int(d) == W.wf_distance(a, p) % 32
+                                              for d, p in zip(dists, plains)),
+                          "note": "one preprocessed encrypted query vs 64 plaintext strings, "
+                                  "all strings' anti-diagonals per launch "
+                                  "(lv_edit_distance_pre_batch); table built once"}
+    ctx.release([r.score for r in runs])
+    ctx.release(xs.chars)
+    del table
     npairs = 256 if full_cfg5 else 16
     pairs = W.cfg5(npairs)
     L.compute_batch(pairs[:2], ctx=ctx)

@@ -167,6 +167,15 @@ void lv_eq_table_destroy(lv_ctx* ctx, lv_eqtable* t);
 /* preprocess::distance_preprocessed (preprocess.cpp:62-76). */
 int lv_edit_distance_pre(lv_ctx* ctx, const lv_eqtable* t, const char* plain, size_t n,
                          const lv_band* band, int32_t key_encoding, lv_ct* score, lv_run* run);
+/* Many plaintext strings against their tables in one wavefront (the
+ * database-scan use of one preprocessed query):
+ * string p = plains[plain_off[p] .. plain_off[p+1]) against tables[p]
+ * (tables may repeat). Every pair's same-index anti-diagonal shares one
+ * launch; scores/runs as lv_edit_distance_pre per pair. */
+int lv_edit_distance_pre_batch(lv_ctx* ctx, size_t npairs, const lv_eqtable* const* tables,
+                               const char* plains, const uint64_t* plain_off,
+                               const lv_band* bands, int32_t key_encoding, lv_ct* scores,
+                               lv_run* runs);
 
 /* Symbolic schedule of a traversal (no device work): per visited cell
  * (i, j, key variance, refreshes before it) — the observer hook of

@@ -117,7 +117,8 @@ EXPORTS = [
     "lv_get_stats", "lv_get_params", "lv_release", "lv_ledger_variance", "lv_export",
     "lv_import", "lv_phase", "lv_pbs_batch_host", "lv_band_resolve", "lv_edit_distance_ee",
     "lv_edit_distance_batch", "lv_eq_table_build", "lv_eq_table_lookup", "lv_eq_table_destroy",
-    "lv_edit_distance_pre", "lv_plan_trace", "lv_debug_keys", "lv_debug_keyswitch",
+    "lv_edit_distance_pre", "lv_edit_distance_pre_batch", "lv_plan_trace", "lv_debug_keys",
+    "lv_debug_keyswitch",
     "lv_eq_table_serialize", "lv_eq_table_deserialize",
     "lv_debug_blind_rotate", "lv_debug_fft", "lv_bench_pbs", "lv_bench_fp64_peak",
 ]
@@ -181,6 +182,8 @@ def lib():
                                                        ctypes.c_void_p, u64, P(u64)]),
             "lv_edit_distance_pre": (ctypes.c_int, [vp, vp, ctypes.c_char_p, sz, P(Band), i32,
                                                     P(u32), P(Run)]),
+            "lv_edit_distance_pre_batch": (ctypes.c_int, [vp, sz, P(vp), ctypes.c_char_p, P(u64),
+                                                          P(Band), i32, P(u32), P(Run)]),
             "lv_plan_trace": (ctypes.c_int, [u64, u64, P(Band), i32, ctypes.c_double, u64, P(u32),
                                              P(i64), P(u32), P(u64), P(Run)]),
             "lv_debug_keys": (ctypes.c_int, [vp, P(ctypes.c_uint8), P(ctypes.c_uint8), P(u64),
@@ -469,15 +472,16 @@ def fp64_peak_tflops() -> float:
 
 from .leuven import (  # noqa: E402  (reference-shaped pipeline API)
     AlphabetSpec, BandSpec, DistanceRun, EqTable, EncryptedString, band_cell_count, build_eq_table,
-    compute, compute_batch, distance_encrypted, distance_preprocessed, encrypt_string, load_eq_table,
-    plan_trace, report_json, run_batch, save_eq_table, wf_distance,
+    compute, compute_batch, distance_encrypted, distance_preprocessed, distance_preprocessed_batch,
+    encrypt_string, load_eq_table, plan_trace, report_json, run_batch, save_eq_table, wf_distance,
 )
 
 __all__ = [
     "Context", "Params", "default_params", "negacyclic_eval", "identity_lut", "eq_lut", "AlphabetSpec",
     "BandSpec", "DistanceRun", "EqTable", "EncryptedString", "band_cell_count", "build_eq_table",
-    "compute", "compute_batch", "distance_encrypted", "distance_preprocessed", "encrypt_string",
-    "plan_trace", "wf_distance", "run_batch", "report_json", "save_eq_table", "load_eq_table", "Error", "OutOfRangeValue", "NoiseBudgetExceeded",
+    "compute", "compute_batch", "distance_encrypted", "distance_preprocessed",
+    "distance_preprocessed_batch", "encrypt_string", "plan_trace", "wf_distance", "run_batch",
+    "report_json", "save_eq_table", "load_eq_table", "Error", "OutOfRangeValue", "NoiseBudgetExceeded",
     "ValueOutsideLutHalf", "PackingViolation", "CharNotInAlphabet", "CharNotInSubset",
     "PositionOutOfRange", "BandTooNarrow", "FormatError", "InvalidParams", "CudaError", "InvalidHandle",
 ]

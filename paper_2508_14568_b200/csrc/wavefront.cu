@@ -632,6 +632,24 @@ int lv_edit_distance_pre(lv_ctx* c, const lv_eqtable* t, const char* plain, size
   });
 }
 
+int lv_edit_distance_pre_batch(lv_ctx* c, size_t npairs, const lv_eqtable* const* tables,
+                               const char* plains, const uint64_t* plain_off,
+                               const lv_band* bands, int32_t key_encoding, lv_ct* scores,
+                               lv_run* runs) {
+  return guard_wf([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    std::vector<PairIn> pairs;
+    pairs.reserve(npairs);
+    for (size_t p = 0; p < npairs; ++p) {
+      if (!tables[p]) throw Error(LV_ERR_INVALID_HANDLE, "null equality table");
+      const uint64_t n = plain_off[p + 1] - plain_off[p];
+      pairs.push_back(PairIn{(uint32_t)tables[p]->length, (uint32_t)n, to_band(&bands[p]), nullptr,
+                             nullptr, tables[p], plains + plain_off[p]});
+    }
+    run_traversals(c, pairs, 0, key_encoding == LV_KEY_NEGATED, scores, runs);
+  });
+}
+
 int lv_plan_trace(uint64_t m, uint64_t n, const lv_band* band, int32_t key_encoding, double budget,
                   uint64_t cap, uint32_t* ij, int64_t* key_var, uint32_t* refreshes,
                   uint64_t* count, lv_run* totals) {

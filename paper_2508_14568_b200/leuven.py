@@ -263,6 +263,30 @@ def distance_preprocessed(ctx: Context, table: EqTable, plain: str, band: BandSp
     return _run(run, score.value)
 
 
+def distance_preprocessed_batch(ctx: Context, tables, plains, bands,
+                                encoding: str = "negated"):
+    """Many plaintext strings against equality tables in one wavefront
+    (lv_edit_distance_pre_batch): the database-scan use of one preprocessed
+    encrypted query. ``tables`` is one EqTable or one
+    per string; ``bands`` one BandSpec or one per string."""
+    n = len(plains)
+    tabs = list(tables) if isinstance(tables, (list, tuple)) else [tables] * n
+    bnds = list(bands) if isinstance(bands, (list, tuple)) else [bands] * n
+    if len(tabs) != n or len(bnds) != n:
+        raise InvalidParams("one table and one band per plaintext string")
+    data = "".join(plains).encode("latin1")
+    off = np.zeros(n + 1, np.uint64)
+    off[1:] = np.cumsum([len(s) for s in plains])
+    th = (ctypes.c_void_p * max(1, n))(*[t._h for t in tabs])
+    bc = (Band * max(1, n))(*[b._c() for b in bnds])
+    scores = np.zeros(max(1, n), np.uint32)
+    runs = (Run * max(1, n))()
+    _check(lib().lv_edit_distance_pre_batch(ctx._h, n, th, data, _ptr(off, ctypes.c_uint64), bc,
+                                            _key_enc(encoding), _ptr(scores, ctypes.c_uint32),
+                                            runs))
+    return [_run(runs[p], scores[p]) for p in range(n)]
+
+
 def plan_trace(m: int, n: int, band: BandSpec, key_encoding: str = "negated",
                budget: float = 4000.0):
     """Per-cell (i, j, key variance, refreshes) of the symbolic schedule."""

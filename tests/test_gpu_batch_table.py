@@ -80,3 +80,26 @@ def test_cli_compute_and_batch(tmp_path, golden):
     err = _io.StringIO()
     assert main(["compute", "--a", "abcdef", "--b", "a", "--mode", "approx", "--ell", "1"],
                 out=_io.StringIO(), err=err) == 3
+
+
+def test_preprocessed_batch_database_scan(ctx):
+    """One preprocessed encrypted query against many plaintext strings in one
+    wavefront equals the per-string distance_preprocessed (distance and every
+    counter) and Wagner-Fischer."""
+    from paper_2508_14568_b200 import workloads as W
+    a, b = W.cfg4()
+    a = a[:24]
+    spec = L.AlphabetSpec.dna4()
+    xs = L.encrypt_string(a, spec, ctx)
+    table, _ = L.build_eq_table(ctx, xs, spec)
+    plains = [b[:20], a, W.mutate(a, 3, W.MT19937(77), draw=W.dna), "ACGT", "", "T" * 30]
+    bands = [L.BandSpec.exact(len(a), len(p)) for p in plains]
+    runs = L.distance_preprocessed_batch(ctx, table, plains, bands)
+    got = ctx.decrypt([r.score for r in runs])
+    for p, band, r, d in zip(plains, bands, runs, got):
+        one = L.distance_preprocessed(ctx, table, p, band)
+        assert d == ctx.decrypt([one.score])[0] == L.wf_distance(a, p) % 32, p
+        assert (r.visited_cells, r.equality_pbs, r.kernel_pbs, r.refreshes, r.max_key_variance) == (
+            one.visited_cells, one.equality_pbs, one.kernel_pbs, one.refreshes, one.max_key_variance)
+    with pytest.raises(L.CharNotInSubset):
+        L.distance_preprocessed_batch(ctx, table, ["ACGX"], [L.BandSpec.exact(len(a), 4)])
