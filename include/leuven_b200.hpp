@@ -247,5 +247,29 @@ inline DistanceRun distance_preprocessed(GpuBackend& be, const EqTable& table,
   return r;
 }
 
+// One table against many plaintext strings, all anti-diagonals batched
+// (lv_edit_distance_pre_batch): the database-scan use of a preprocessed query.
+inline std::vector<DistanceRun> distance_preprocessed_batch(
+    GpuBackend& be, const EqTable& table, const std::vector<std::string>& plains,
+    const std::vector<BandSpec>& bands, KeyEncoding enc = KeyEncoding::negated) {
+  if (bands.size() != plains.size()) throw InvalidParams("one band per plaintext string");
+  std::string data;
+  std::vector<uint64_t> off(1, 0);
+  std::vector<const lv_eqtable*> tables(plains.size(), table.raw());
+  std::vector<lv_band> b;
+  for (size_t p = 0; p < plains.size(); ++p) {
+    data += plains[p];
+    off.push_back(data.size());
+    b.push_back(bands[p].b);
+  }
+  std::vector<lv_ct> scores(plains.size());
+  std::vector<lv_run> runs(plains.size());
+  check(lv_edit_distance_pre_batch(be.raw(), plains.size(), tables.data(), data.data(), off.data(),
+                                   b.data(), static_cast<int32_t>(enc), scores.data(), runs.data()));
+  std::vector<DistanceRun> out(plains.size());
+  for (size_t p = 0; p < plains.size(); ++p) out[p] = DistanceRun{scores[p], runs[p]};
+  return out;
+}
+
 }  // namespace b200
 }  // namespace leuven

@@ -98,6 +98,12 @@ int main() {
     CHECK(b.decrypt(r.score) == 1);
     CHECK(r.counters.equality_pbs == 0);
     CHECK(r.counters.kernel_pbs == 56);
+    const std::vector<DistanceRun> scan = distance_preprocessed_batch(
+        b, *t, {"ACGTGCA", "ACGTACGT", "T"},
+        {BandSpec::exact(8, 7), BandSpec::exact(8, 8), BandSpec::exact(8, 1)});
+    CHECK(scan.size() == 3);
+    CHECK(b.decrypt(scan[0].score) == 1);
+    CHECK(scan[0].counters.kernel_pbs == 56);
     delete t;
   }
   std::printf("%s: %d failures\n", g_fail ? "FAILED" : "OK", g_fail);
