@@ -176,9 +176,8 @@ static void launch_keyswitch(lv_ctx* c, const LinDesc* d_desc, uint32_t count, u
   LV_CUDA(cudaGetLastError());
 }
 
-// Waves of at most br_pair_max items (default: half the SMs) leave SMs idle
-// in the single-CTA form; they run the CTA-pair form instead, two SMs per
-// item.
+// Waves of at most br_pair_max items (default: one per SM) leave SMs idle in
+// the single-CTA form; they run the CTA-pair form instead (2 CTAs per item).
 void launch_blind_rotate(lv_ctx* c, const BrArgs& ba, uint32_t count) {
   if (!count) return;
   if (count <= c->br_pair_max)
@@ -511,7 +510,7 @@ int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
       {
         int sms = 148;
         LV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-        c->br_pair_max = (uint32_t)sms / 2;
+        c->br_pair_max = (uint32_t)sms;
         if (const char* e = std::getenv("LVB_BR_PAIR_MAX"))
           c->br_pair_max = (uint32_t)std::strtoul(e, nullptr, 10);
       }
