@@ -203,9 +203,9 @@ size_t blind_rotate_smem_bytes(uint32_t n) {
 // Latency form of the blind rotation for waves too small to fill the GPU:
 // a cluster of 2 CTAs per item, CTA p owning GLWE
 // polynomial p (0 = mask, 1 = body). Per CMUX each CTA decomposes and
-// transforms its own polynomial, publishes the spectrum in its shared
-// memory, and after a cluster barrier reads the partner's spectrum through
-// distributed shared memory to form its own output o = p:
+// transforms its own polynomial, stores the spectrum into the partner's
+// shared memory (distributed shared memory), and after a cluster barrier
+// reads the partner's spectrum locally to form its own output o = p:
 // D0 * BSK[0][o] + D1 * BSK[1][o] (the single-CTA kernel's FMA order, so
 // results are bit-identical), then inverse-transforms and accumulates it.
 namespace cg = cooperative_groups;
@@ -219,7 +219,7 @@ blind_rotate_pair_kernel(BrArgs a) {
   uint16_t* ms = reinterpret_cast<uint16_t*>(smem + kN * 8 + 3 * kM * 16);
   cg::cluster_group cluster = cg::this_cluster();
   const uint32_t p = cluster.block_rank();
-  const double2* pspec = cluster.map_shared_rank(spec, p ^ 1u);
+  double2* pspec = cluster.map_shared_rank(spec, p ^ 1u);  // the partner's inbox
   const uint32_t t = threadIdx.x;
   const uint32_t item = blockIdx.x >> 1;
   const uint32_t n = a.n;
@@ -251,10 +251,10 @@ blind_rotate_pair_kernel(BrArgs a) {
   }
   cluster.sync();  // the partner's shared memory is live before any DSMEM access
 
-  // The published spectrum alternates between two buffers by executed-CMUX
-  // parity, so the one cluster barrier per CMUX (after publishing) also
-  // guarantees the partner finished reading the buffer being overwritten
-  // (it read it two CMUXes ago, before arriving at the last barrier).
+  // The inbox alternates between two buffers by executed-CMUX parity, so the
+  // one cluster barrier per CMUX (after delivering) also guarantees the
+  // partner finished reading the buffer being overwritten (it read it two
+  // CMUXes ago, before arriving at the last barrier).
   uint32_t parity = 0;
   for (uint32_t i = 0; i < n; ++i) {
     __syncthreads();  // previous update of acc visible to the rotated reads
@@ -287,12 +287,14 @@ blind_rotate_pair_kernel(BrArgs a) {
       X[0][r] = cmul(make_double2((double)d[0], (double)d[1]), tz[r]);
     }
     fft_forward<1>(X, buf, tw, t);
-    double2* mine = spec + parity * kM;
+    // push the spectrum into the partner's inbox (remote stores, no latency
+    // on this side); the barrier's release/acquire makes them visible
+    double2* theirs = pspec + parity * kM;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) mine[q * 128 + t] = X[0][q];
-    cluster.sync();  // both spectra published
+    for (int q = 0; q < 8; ++q) theirs[q * 128 + t] = X[0][q];
+    cluster.sync();  // both spectra delivered
     {
-      const double2* other_spec = pspec + parity * kM;
+      const double2* other_spec = spec + parity * kM;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const double2 other = other_spec[q * 128 + t];

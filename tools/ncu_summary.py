@@ -46,7 +46,11 @@ KEYS = [
     "l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate.pct",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
-    "sm__inst_executed.sum", "launch__registers_per_thread", "launch__occupancy_limit_shared_mem",
+    "sm__inst_executed.sum", "sm__inst_executed.avg.per_cycle_active",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "launch__registers_per_thread", "launch__occupancy_limit_shared_mem",
+    "launch__occupancy_limit_registers", "launch__grid_size", "launch__cluster_dim_x",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
     "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct",
     "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
