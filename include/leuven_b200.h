@@ -57,6 +57,12 @@ typedef struct {
   uint32_t lwe_noise_log2;    /* TUniform bound, small-key LWE (KSK) noise   */
   uint32_t glwe_noise_log2;   /* TUniform bound, GLWE / fresh big-key noise  */
   double max_variance_budget; /* NoiseParams::max_variance_budget, backend.hpp:23-34 */
+  uint32_t exact_mask_product; /* 0: one f64 FFT product per external-product output
+                                * (default); 1: the mask output splits the BSK as
+                                * H 2^43 + Lo with an exactly rounded H product, so
+                                * the FFT adds no key-amplified noise (phase-noise
+                                * variance within 1.001x of exact integer products;
+                                * 1.47x blind-rotation time). DESIGN.md §2. */
 } lv_params;
 
 typedef struct lv_ctx lv_ctx;

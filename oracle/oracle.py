@@ -26,6 +26,7 @@ class Params(ctypes.Structure):
         ("ks_level", ctypes.c_uint32),
         ("lwe_noise_log2", ctypes.c_uint32),
         ("glwe_noise_log2", ctypes.c_uint32),
+        ("exact_mask_product", ctypes.c_uint32),
     ]
 
     def as_dict(self):
@@ -62,7 +63,9 @@ def lib():
         for name, rt in (("orc_sk_small", ctypes.POINTER(ctypes.c_uint8)),
                          ("orc_sk_glwe", ctypes.POINTER(ctypes.c_uint8)),
                          ("orc_ksk", u64p), ("orc_bsk", u64p),
-                         ("orc_bskf", ctypes.POINTER(ctypes.c_double))):
+                         ("orc_bskf", ctypes.POINTER(ctypes.c_double)),
+                         ("orc_bskf_hi", ctypes.POINTER(ctypes.c_double)),
+                         ("orc_bskf_lo", ctypes.POINTER(ctypes.c_double))):
             getattr(L, name).restype = rt
             getattr(L, name).argtypes = [vp]
         L.orc_encrypt_at.argtypes = [vp, ctypes.c_int32, ctypes.c_uint64, u64p]
@@ -139,6 +142,12 @@ class Oracle:
 
     def bskf(self):
         return np.ctypeslib.as_array(lib().orc_bskf(self._c), (self.n * self.rows * (self.k + 1) * self.N,)).copy()
+
+    def bskf_split(self):
+        """(H, Lo) spectra of the mask polynomials (exact_mask_product keys)."""
+        size = (self.n * self.rows * self.k * self.N,)
+        return (np.ctypeslib.as_array(lib().orc_bskf_hi(self._c), size).copy(),
+                np.ctypeslib.as_array(lib().orc_bskf_lo(self._c), size).copy())
 
     # ciphertexts ----------------------------------------------------
     def encrypt(self, value: int, counter: int) -> np.ndarray:

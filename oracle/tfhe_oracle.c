@@ -43,6 +43,8 @@ struct orc_ctx {
   uint64_t* ksk;
   uint64_t* bsk;
   double* bskf;    /* interleaved (re, im) */
+  double* bskf_hi; /* exact_mask_product: spectra of H and Lo of every mask */
+  double* bskf_lo; /* polynomial, [(i * rows + r) * k + q][2M]             */
   double* tw;      /* W[t] = exp(-2 pi i t / M), t < M/2, interleaved */
   double* twist;   /* zeta^j = exp(i pi j / N), j < M */
   double* untwist; /* zeta^-j / M */
@@ -110,6 +112,7 @@ orc_params orc_default_params(void) {
   p.ks_level = 5;
   p.lwe_noise_log2 = 44;
   p.glwe_noise_log2 = 17;
+  p.exact_mask_product = 0;
   return p;
 }
 
@@ -482,6 +485,21 @@ static void bsk_range(void* a, size_t lo, size_t hi) {
         forward_i64_dd(c, tmp, spec, work);
         memcpy(c->bskf + (((size_t)i * rows + r) * (k + 1) + o) * 2 * c->M, spec,
                sizeof(double) * 2 * c->M);
+        if (p->exact_mask_product && o < k) {
+          /* b = H * 2^43 + Lo, H = round(b / 2^43) (signed, mod 2^64) */
+          int64_t* lo = (int64_t*)malloc(sizeof(int64_t) * N);
+          for (uint32_t cc = 0; cc < N; ++cc) {
+            const int64_t h = (int64_t)(poly[cc] + (UINT64_C(1) << 42)) >> 43;
+            tmp[cc] = h;
+            lo[cc] = (int64_t)(poly[cc] - ((uint64_t)h << 43));
+          }
+          const size_t slot = (((size_t)i * rows + r) * k + o) * 2 * c->M;
+          forward_i64_dd(c, tmp, spec, work);
+          memcpy(c->bskf_hi + slot, spec, sizeof(double) * 2 * c->M);
+          forward_i64_dd(c, lo, spec, work);
+          memcpy(c->bskf_lo + slot, spec, sizeof(double) * 2 * c->M);
+          free(lo);
+        }
       }
     }
   }
@@ -522,6 +540,10 @@ orc_ctx* orc_create(const orc_params* p, uint64_t seed, int threads) {
   for (uint32_t j = 0; j < k * N; ++j) c->sk_glwe[j] = (uint8_t)(orc_rand_u64(seed, D_SK_GLWE, j) & 1);
   c->bsk = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n * rows * (k + 1) * N);
   c->bskf = (double*)malloc(sizeof(double) * (size_t)n * rows * (k + 1) * N);
+  if (p->exact_mask_product) {
+    c->bskf_hi = (double*)malloc(sizeof(double) * (size_t)n * rows * k * N);
+    c->bskf_lo = (double*)malloc(sizeof(double) * (size_t)n * rows * k * N);
+  }
   c->ksk = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)k * N * p->ks_level * (n + 1));
   keygen_arg ka = {c};
   parallel_for(n, threads, bsk_range, &ka);
@@ -535,6 +557,8 @@ void orc_destroy(orc_ctx* c) {
   free(c->sk_glwe);
   free(c->bsk);
   free(c->bskf);
+  free(c->bskf_hi);
+  free(c->bskf_lo);
   free(c->ksk);
   free(c->tw);
   free(c->twist);
@@ -550,6 +574,8 @@ const uint8_t* orc_sk_glwe(const orc_ctx* c) { return c->sk_glwe; }
 const uint64_t* orc_ksk(const orc_ctx* c) { return c->ksk; }
 const uint64_t* orc_bsk(const orc_ctx* c) { return c->bsk; }
 const double* orc_bskf(const orc_ctx* c) { return c->bskf; }
+const double* orc_bskf_hi(const orc_ctx* c) { return c->bskf_hi; }
+const double* orc_bskf_lo(const orc_ctx* c) { return c->bskf_lo; }
 
 /* ------------------------------------------------------------------ */
 /* encryption                                                           */
@@ -634,6 +660,21 @@ void orc_test_poly(const orc_ctx* c, const int32_t lut[16], uint64_t* tp) {
   }
 }
 
+/* acc += d * b per bin, the MAC's fixed FMA order (blind_rotate_kernel) */
+static void mac_bins(double* acc, const double* d, const double* b, uint32_t M) {
+  for (uint32_t f = 0; f < M; ++f) {
+    double ar = acc[2 * f], ai = acc[2 * f + 1];
+    const double dr = d[2 * f], di = d[2 * f + 1];
+    const double br = b[2 * f], bi = b[2 * f + 1];
+    ar = fma(dr, br, ar);
+    ar = fma(-di, bi, ar);
+    ai = fma(dr, bi, ai);
+    ai = fma(di, br, ai);
+    acc[2 * f] = ar;
+    acc[2 * f + 1] = ai;
+  }
+}
+
 static void external_product_fft(const orc_ctx* c, size_t i, const uint64_t* glwe_in,
                                  uint64_t* glwe_out, double* specs /* rows*2M */,
                                  double* acc /* 2M */, int64_t* dig /* L*N */) {
@@ -650,6 +691,22 @@ static void external_product_fft(const orc_ctx* c, size_t i, const uint64_t* glw
       forward_i64(c, dig + (size_t)l * N, specs + (size_t)(comp * L + l) * 2 * M);
   }
   for (uint32_t o = 0; o <= k; ++o) {
+    if (p->exact_mask_product && o < k) {
+      /* mask output: 2^43 * round(sum d * H) + sum d * Lo */
+      uint64_t* hi = (uint64_t*)malloc(sizeof(uint64_t) * N);
+      for (int part = 0; part < 2; ++part) {
+        memset(acc, 0, sizeof(double) * 2 * M);
+        for (uint32_t r = 0; r < rows; ++r) {
+          const double* d = specs + (size_t)r * 2 * M;
+          const double* b = (part == 0 ? c->bskf_hi : c->bskf_lo) + ((i * rows + r) * k + o) * 2 * M;
+          mac_bins(acc, d, b, M);
+        }
+        backward_torus(c, acc, part == 0 ? hi : glwe_out + (size_t)o * N);
+      }
+      for (uint32_t j = 0; j < N; ++j) glwe_out[(size_t)o * N + j] += hi[j] << 43;
+      free(hi);
+      continue;
+    }
     memset(acc, 0, sizeof(double) * 2 * M);
     for (uint32_t r = 0; r < rows; ++r) {
       const double* d = specs + (size_t)r * 2 * M;

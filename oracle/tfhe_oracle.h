@@ -48,6 +48,11 @@ typedef struct {
   uint32_t ks_level;
   uint32_t lwe_noise_log2;  /* TUniform bound log2 for small-key LWE noise */
   uint32_t glwe_noise_log2; /* TUniform bound log2 for GLWE / big-key noise*/
+  /* 1: the mask output of every external product splits the BSK mask
+   * coefficients b = H * 2^43 + Lo (|H| <= 2^20, |Lo| <= 2^42); the H
+   * product is exact in f64 and rounded to an integer, so the FFT adds no
+   * noise that the key amplifies. 0: one f64 product. */
+  uint32_t exact_mask_product;
 } orc_params;
 
 typedef struct orc_ctx orc_ctx;
@@ -71,6 +76,8 @@ const uint8_t* orc_sk_glwe(const orc_ctx* c);    /* k*N                   */
 const uint64_t* orc_ksk(const orc_ctx* c);       /* kN*ks_level*(n+1)     */
 const uint64_t* orc_bsk(const orc_ctx* c);       /* n*rows*(k+1)*N        */
 const double* orc_bskf(const orc_ctx* c);        /* n*rows*(k+1)*(N/2)*2 (re,im interleaved) */
+const double* orc_bskf_hi(const orc_ctx* c);     /* exact_mask_product: n*rows*k*(N/2)*2     */
+const double* orc_bskf_lo(const orc_ctx* c);     /* (NULL otherwise)                          */
 
 /* Big-key LWE: kN mask coefficients followed by the body (kN+1 u64). */
 void orc_encrypt_at(const orc_ctx* c, int32_t value, uint64_t counter, uint64_t* out);

@@ -91,7 +91,7 @@ class Params(ctypes.Structure):
                 ("pbs_base_log", ctypes.c_uint32), ("pbs_level", ctypes.c_uint32),
                 ("ks_base_log", ctypes.c_uint32), ("ks_level", ctypes.c_uint32),
                 ("lwe_noise_log2", ctypes.c_uint32), ("glwe_noise_log2", ctypes.c_uint32),
-                ("max_variance_budget", ctypes.c_double)]
+                ("max_variance_budget", ctypes.c_double), ("exact_mask_product", ctypes.c_uint32)]
 
 
 class Stats(ctypes.Structure):

@@ -178,12 +178,16 @@ static void launch_keyswitch(lv_ctx* c, const LinDesc* d_desc, uint32_t count, u
 
 // Waves of at most br_pair_max items (default: one per SM) leave SMs idle in
 // the single-CTA form; they run the CTA-pair form instead (2 CTAs per item).
+// Keys with exact_mask_product use the single-CTA exact-mask form at every
+// size.
 void launch_blind_rotate(lv_ctx* c, const BrArgs& ba, uint32_t count) {
   if (!count) return;
-  if (count <= c->br_pair_max)
+  if (c->p.exact_mask_product)
+    blind_rotate_exact_kernel<<<count, 128, blind_rotate_smem_bytes(c->p.n, true), c->stream>>>(ba);
+  else if (count <= c->br_pair_max)
     blind_rotate_pair_kernel<<<2 * count, 128, blind_rotate_pair_smem_bytes(c->p.n), c->stream>>>(ba);
   else
-    blind_rotate_kernel<<<count, 128, blind_rotate_smem_bytes(c->p.n), c->stream>>>(ba);
+    blind_rotate_kernel<<<count, 128, blind_rotate_smem_bytes(c->p.n, false), c->stream>>>(ba);
   LV_CUDA(cudaGetLastError());
 }
 
@@ -395,7 +399,9 @@ static void keygen(lv_ctx* c) {
   keygen_bsk_kernel<<<n * kRows, 256, 0, c->stream>>>(c->seed, c->p.glwe_noise_log2, c->d_sk_small,
                                                       c->d_sk_glwe, d_bsk);
   LV_CUDA(cudaGetLastError());
-  LV_CUDA(cudaMalloc(&c->d_bskf, (size_t)n * 32 * 128 * sizeof(double2)));
+  const bool exact = c->p.exact_mask_product != 0;
+  const uint32_t nouts = exact ? 3 : 2;  // spectra per GGSW row: [mask, body] or [H, Lo, body]
+  LV_CUDA(cudaMalloc(&c->d_bskf, (size_t)n * 8 * kRows * nouts * 128 * sizeof(double2)));
   // double-double twiddle / twist tables for the BSK transform (oracle
   // build_tables: hi = rn(v), lo = rn(v - hi) from long double)
   std::vector<double4> tw_dd(kM / 2), twist_dd(kM);
@@ -420,12 +426,20 @@ static void keygen(lv_ctx* c) {
   LV_CUDA(cudaMemcpy(d_tw_dd, tw_dd.data(), tw_dd.size() * sizeof(double4), cudaMemcpyHostToDevice));
   LV_CUDA(cudaMemcpy(d_twist_dd, twist_dd.data(), twist_dd.size() * sizeof(double4),
                      cudaMemcpyHostToDevice));
-  bsk_fourier_kernel<<<n * kRows * 2, 512, 0, c->stream>>>(d_bsk, d_tw_dd, d_twist_dd, c->d_bskf);
+  uint64_t* d_split = nullptr;
+  if (exact) {
+    LV_CUDA(cudaMalloc(&d_split, (size_t)n * kRows * 3 * kN * sizeof(uint64_t)));
+    bsk_split_kernel<<<n * kRows, 256, 0, c->stream>>>(d_bsk, d_split);
+    LV_CUDA(cudaGetLastError());
+  }
+  bsk_fourier_kernel<<<n * kRows * nouts, 512, 0, c->stream>>>(exact ? d_split : d_bsk, nouts,
+                                                                d_tw_dd, d_twist_dd, c->d_bskf);
   LV_CUDA(cudaGetLastError());
   LV_CUDA(cudaStreamSynchronize(c->stream));
   LV_CUDA(cudaFree(d_bsk));
   LV_CUDA(cudaFree(d_tw_dd));
   LV_CUDA(cudaFree(d_twist_dd));
+  if (d_split) LV_CUDA(cudaFree(d_split));
 }
 
 std::array<int32_t, 16> eq_lut_entries(int scale) {  // equality.cpp:31-36
@@ -473,6 +487,7 @@ void lv_default_params(lv_params* p) {
   p->lwe_noise_log2 = 44;
   p->glwe_noise_log2 = 17;
   p->max_variance_budget = 4000.0;
+  p->exact_mask_product = 0;
 }
 
 const char* lv_last_error(void) { return g_last_error.c_str(); }
@@ -500,8 +515,12 @@ int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
       c->seed = seed;
       LV_CUDA(cudaGetDevice(&c->device));
       LV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-      LV_CUDA(cudaFuncSetAttribute(blind_rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)blind_rotate_smem_bytes(p.n)));
+      LV_CUDA(cudaFuncSetAttribute(blind_rotate_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)blind_rotate_smem_bytes(p.n, false)));
+      LV_CUDA(cudaFuncSetAttribute(blind_rotate_exact_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)blind_rotate_smem_bytes(p.n, true)));
       LV_CUDA(cudaFuncSetAttribute(ks_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)ks_tc_smem_bytes()));
       LV_CUDA(cudaFuncSetAttribute(blind_rotate_pair_kernel,
@@ -799,6 +818,8 @@ int lv_debug_keys(lv_ctx* c, uint8_t* sk_small, uint8_t* sk_glwe, uint64_t* ksk,
     if (sk_glwe) LV_CUDA(cudaMemcpy(sk_glwe, c->d_sk_glwe, kBig, cudaMemcpyDeviceToHost));
     if (ksk)
       LV_CUDA(cudaMemcpy(ksk, c->d_ksk, (size_t)kBig * kKsLevel * (n + 1) * 8, cudaMemcpyDeviceToHost));
+    if (bskf_nat && c->p.exact_mask_product)
+      throw Error(LV_ERR_INVALID_PARAMS, "debug_keys: exact_mask_product keys use the split layout");
     if (bskf_nat) {
       std::vector<double2> raw((size_t)n * 32 * 128);
       LV_CUDA(cudaMemcpy(raw.data(), c->d_bskf, raw.size() * sizeof(double2), cudaMemcpyDeviceToHost));

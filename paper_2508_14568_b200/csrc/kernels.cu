@@ -36,14 +36,35 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
 }
 
 // ------------------------------------------------------------------ BR
+// o = d0 * b0 + d1 * b1 for one spectrum bin, in the MAC's fixed FMA order
+// (oracle mac_bins): row 0 then row 1, real part first.
+__device__ __forceinline__ double2 mac2(double2 d0, double2 b0, double2 d1, double2 b1) {
+  double2 o;
+  o.x = __fma_rn(d0.x, b0.x, 0.0);
+  o.x = __fma_rn(-d0.y, b0.y, o.x);
+  o.y = __fma_rn(d0.x, b0.y, 0.0);
+  o.y = __fma_rn(d0.y, b0.x, o.y);
+  o.x = __fma_rn(d1.x, b1.x, o.x);
+  o.x = __fma_rn(-d1.y, b1.y, o.x);
+  o.y = __fma_rn(d1.x, b1.y, o.y);
+  o.y = __fma_rn(d1.y, b1.x, o.y);
+  return o;
+}
+
 // One CTA (128 threads) blind-rotates one item: ACC = X^{-b~} (0, TP), then
 // for every small-key coefficient i: ACC += BSK_i [x] (X^{a~_i} ACC - ACC),
 // then sample-extracts coefficient 0 into a big-key LWE.
 //
+// kExact (lv_params.exact_mask_product): the mask output of each external
+// product is 2^43 * round(D * H) + D * Lo with the BSK mask split
+// b = H 2^43 + Lo; the H product is exact in f64, so the FFT adds no noise
+// that the secret key amplifies. Costs a third inverse transform per CMUX
+// (three spectra inverted in lockstep; 2 CTAs/SM for the registers).
+//
 // Shared memory: acc[2][N] u64 (32 KB) + FFT exchange buffer kXchgBufs x kM
-// double2 (16 KB split / 32 KB) + ms[n+1] u16. 168 registers, 3 CTAs/SM.
-__global__ void __launch_bounds__(128, 3)
-blind_rotate_kernel(BrArgs a) {
+// double2 (16 KB) + ms[n+1] u16. 168 registers, 3 CTAs/SM.
+template <bool kExact>
+__device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* acc = reinterpret_cast<uint64_t*>(smem);                   // [2][kN]
   double2* buf = reinterpret_cast<double2*>(smem + 2 * kN * 8);        // [kXchgBufs][kM]
@@ -111,55 +132,71 @@ blind_rotate_kernel(BrArgs a) {
 
     fft_forward<2>(X, buf, tw, t);
 
-    // pointwise MAC against BSK_i (bins 8t + q), layout [i][q*4 + row*2 + o][t]
-    {
-      const double2* bsk = a.bskf + (size_t)i * (32 * 128) + t;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double2 b00 = ld_stream(bsk + (q * 4 + 0) * 128);
-        const double2 b01 = ld_stream(bsk + (q * 4 + 1) * 128);
-        const double2 b10 = ld_stream(bsk + (q * 4 + 2) * 128);
-        const double2 b11 = ld_stream(bsk + (q * 4 + 3) * 128);
-        const double2 d0 = X[0][q], d1 = X[1][q];
-        double2 o0, o1;
-        o0.x = __fma_rn(d0.x, b00.x, 0.0);
-        o0.x = __fma_rn(-d0.y, b00.y, o0.x);
-        o0.y = __fma_rn(d0.x, b00.y, 0.0);
-        o0.y = __fma_rn(d0.y, b00.x, o0.y);
-        o0.x = __fma_rn(d1.x, b10.x, o0.x);
-        o0.x = __fma_rn(-d1.y, b10.y, o0.x);
-        o0.y = __fma_rn(d1.x, b10.y, o0.y);
-        o0.y = __fma_rn(d1.y, b10.x, o0.y);
-        o1.x = __fma_rn(d0.x, b01.x, 0.0);
-        o1.x = __fma_rn(-d0.y, b01.y, o1.x);
-        o1.y = __fma_rn(d0.x, b01.y, 0.0);
-        o1.y = __fma_rn(d0.y, b01.x, o1.y);
-        o1.x = __fma_rn(d1.x, b11.x, o1.x);
-        o1.x = __fma_rn(-d1.y, b11.y, o1.x);
-        o1.y = __fma_rn(d1.x, b11.y, o1.y);
-        o1.y = __fma_rn(d1.y, b11.x, o1.y);
-        X[0][q] = o0;
-        X[1][q] = o1;
-      }
-    }
-    __syncthreads();  // forward's last buffer reads precede the inverse's writes
-    fft_inverse_a<2>(X, buf, tw, t);
+    // pointwise MAC against BSK_i (bins 8t + q), then the inverse transforms;
     // untwist (conj(twist); the 1/M is pre-applied to the BSK), back to the
     // torus, accumulate into the owned coefficients and publish them
+    if constexpr (kExact) {
+      // layout [i][q*6 + row*3 + o'][t], o' = H, Lo, body; three spectra
+      // inverted in lockstep; mask = acc + 2^43 * round(hi) + lo
+      // (|hi| < 2^53, where f64_to_torus is rint)
+      double2 Z[3][8];
+      const double2* bsk = a.bskf + (size_t)i * (8 * 6 * 128) + t;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const double2 tv = r == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]);
-      const double2 ut = make_double2(tv.x, -tv.y);
-      const uint32_t x = t + 128 * r;
+      for (int q = 0; q < 8; ++q) {
+        const double2* bq = bsk + q * (6 * 128);
+        const double2 d0 = X[0][q], d1 = X[1][q];
+        const double2 h0 = ld_stream(bq), l0 = ld_stream(bq + 128), b0 = ld_stream(bq + 256);
+        const double2 h1 = ld_stream(bq + 384), l1 = ld_stream(bq + 512), b1 = ld_stream(bq + 640);
+        Z[0][q] = mac2(d0, h0, d1, h1);
+        Z[1][q] = mac2(d0, l0, d1, l1);
+        Z[2][q] = mac2(d0, b0, d1, b1);
+      }
+      __syncthreads();  // forward's last buffer reads precede the inverse's writes
+      fft_inverse_a<3>(Z, buf, tw, t);
 #pragma unroll
-      for (int p = 0; p < 2; ++p) {
-        const double2 z = cmul(X[p][r], ut);
-        // re-read (unchanged during the CMUX) instead of holding 64 registers
-        // across the FFTs
-        own[p][2 * r] = acc[p * kN + x] + f64_to_torus(z.x);
-        own[p][2 * r + 1] = acc[p * kN + x + kM] + f64_to_torus(z.y);
-        acc[p * kN + x] = own[p][2 * r];
-        acc[p * kN + x + kM] = own[p][2 * r + 1];
+      for (int r = 0; r < 8; ++r) {
+        const double2 tv = r == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]);
+        const double2 ut = make_double2(tv.x, -tv.y);
+        const uint32_t x = t + 128 * r;
+        const double2 zh = cmul(Z[0][r], ut), zl = cmul(Z[1][r], ut), zb = cmul(Z[2][r], ut);
+        own[0][2 * r] = acc[x] + (f64_to_torus(zh.x) << 43) + f64_to_torus(zl.x);
+        own[0][2 * r + 1] = acc[x + kM] + (f64_to_torus(zh.y) << 43) + f64_to_torus(zl.y);
+        own[1][2 * r] = acc[kN + x] + f64_to_torus(zb.x);
+        own[1][2 * r + 1] = acc[kN + x + kM] + f64_to_torus(zb.y);
+        acc[x] = own[0][2 * r];
+        acc[x + kM] = own[0][2 * r + 1];
+        acc[kN + x] = own[1][2 * r];
+        acc[kN + x + kM] = own[1][2 * r + 1];
+      }
+    } else {
+      // layout [i][q*4 + row*2 + o][t]
+      const double2* bsk = a.bskf + (size_t)i * (8 * 4 * 128) + t;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double2* bq = bsk + q * (4 * 128);
+        const double2 d0 = X[0][q], d1 = X[1][q];
+        const double2 b00 = ld_stream(bq), b01 = ld_stream(bq + 128);
+        const double2 b10 = ld_stream(bq + 256), b11 = ld_stream(bq + 384);
+        X[0][q] = mac2(d0, b00, d1, b10);
+        X[1][q] = mac2(d0, b01, d1, b11);
+      }
+      __syncthreads();  // forward's last buffer reads precede the inverse's writes
+      fft_inverse_a<2>(X, buf, tw, t);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const double2 tv = r == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]);
+        const double2 ut = make_double2(tv.x, -tv.y);
+        const uint32_t x = t + 128 * r;
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const double2 z = cmul(X[p][r], ut);
+          // re-read (unchanged during the CMUX) instead of holding 64
+          // registers across the FFTs
+          own[p][2 * r] = acc[p * kN + x] + f64_to_torus(z.x);
+          own[p][2 * r + 1] = acc[p * kN + x + kM] + f64_to_torus(z.y);
+          acc[p * kN + x] = own[p][2 * r];
+          acc[p * kN + x + kM] = own[p][2 * r + 1];
+        }
       }
     }
   }
@@ -194,8 +231,14 @@ blind_rotate_kernel(BrArgs a) {
     }
   }
 }
+__global__ void __launch_bounds__(128, 3) blind_rotate_kernel(BrArgs a) {
+  blind_rotate_body<false>(a);
+}
+__global__ void __launch_bounds__(128, 2) blind_rotate_exact_kernel(BrArgs a) {
+  blind_rotate_body<true>(a);
+}
 
-size_t blind_rotate_smem_bytes(uint32_t n) {
+size_t blind_rotate_smem_bytes(uint32_t n, bool) {
   return 2 * kN * 8 + kXchgBufs * kM * 16 + ((n + 1) * 2 + 15) / 16 * 16;
 }
 
@@ -659,13 +702,13 @@ __device__ __forceinline__ cdd_t cdd_load(const double4* t, uint32_t k) {
 }
 
 __global__ void __launch_bounds__(512)
-bsk_fourier_kernel(const uint64_t* bsk, const double4* __restrict__ tw_dd,
+bsk_fourier_kernel(const uint64_t* polys, uint32_t nouts, const double4* __restrict__ tw_dd,
                    const double4* __restrict__ twist_dd, double2* bskf) {
   __shared__ cdd_t x[kM];
   const uint32_t t = threadIdx.x;
-  const uint32_t o = blockIdx.x & 1, rowi = blockIdx.x >> 1;  // rowi = i * kRows + r
+  const uint32_t o = blockIdx.x % nouts, rowi = blockIdx.x / nouts;  // rowi = i * kRows + r
   const uint32_t i = rowi / kRows, r = rowi % kRows;
-  const uint64_t* poly = bsk + ((uint64_t)rowi * (kK + 1) + o) * kN;
+  const uint64_t* poly = polys + ((uint64_t)rowi * nouts + o) * kN;
   for (uint32_t j = t; j < kM; j += blockDim.x)
     x[j] = cdd_mul({dd_from_i64(poly[j]), dd_from_i64(poly[j + kM])}, cdd_load(twist_dd, j));
   __syncthreads();
@@ -679,8 +722,23 @@ bsk_fourier_kernel(const uint64_t* bsk, const double4* __restrict__ tw_dd,
   }
   for (uint32_t f = t; f < kM; f += blockDim.x) {
     const double re = __dadd_rn(x[f].re.hi, x[f].re.lo), im = __dadd_rn(x[f].im.hi, x[f].im.lo);
-    bskf[(size_t)i * (32 * 128) + ((f & 7) * 4 + r * 2 + o) * 128 + (f >> 3)] =
-        make_double2(__dmul_rn(re, 0x1p-10), __dmul_rn(im, 0x1p-10));
+    bskf[(size_t)i * (8 * kRows * nouts * 128) + ((f & 7) * kRows * nouts + r * nouts + o) * 128 +
+         (f >> 3)] = make_double2(__dmul_rn(re, 0x1p-10), __dmul_rn(im, 0x1p-10));
+  }
+}
+
+// exact_mask_product keys: per GGSW row, [H, Lo, body] with the mask
+// coefficient b = H 2^43 + Lo, H = round(b / 2^43) (oracle bsk_range).
+__global__ void bsk_split_kernel(const uint64_t* bsk, uint64_t* split) {
+  const uint32_t rowi = blockIdx.x;
+  const uint64_t* mask = bsk + (size_t)rowi * 2 * kN;
+  uint64_t* out = split + (size_t)rowi * 3 * kN;
+  for (uint32_t j = threadIdx.x; j < kN; j += blockDim.x) {
+    const uint64_t b = mask[j];
+    const int64_t h = (int64_t)(b + (1ull << 42)) >> 43;
+    out[j] = (uint64_t)h;
+    out[kN + j] = b - ((uint64_t)h << 43);
+    out[2 * kN + j] = mask[kN + j];
   }
 }
 

@@ -99,8 +99,9 @@ struct PhaseArgs {
   uint64_t* phase;
 };
 
-__global__ void blind_rotate_kernel(BrArgs a);
-size_t blind_rotate_smem_bytes(uint32_t n);
+__global__ void blind_rotate_kernel(BrArgs a);        // lv_params.exact_mask_product = 0
+__global__ void blind_rotate_exact_kernel(BrArgs a);  // lv_params.exact_mask_product = 1
+size_t blind_rotate_smem_bytes(uint32_t n, bool exact);
 __global__ void blind_rotate_pair_kernel(BrArgs a);
 size_t blind_rotate_pair_smem_bytes(uint32_t n);
 __global__ void keyswitch_kernel(KsArgs a);
@@ -113,8 +114,9 @@ __global__ void keygen_ksk_kernel(uint64_t seed, uint32_t n, uint32_t noise_log2
                                   const uint8_t* sk_small, const uint8_t* sk_glwe, uint64_t* ksk);
 __global__ void keygen_bsk_kernel(uint64_t seed, uint32_t noise_log2, const uint8_t* sk_small,
                                   const uint8_t* sk_glwe, uint64_t* bsk);
-__global__ void bsk_fourier_kernel(const uint64_t* bsk, const double4* tw_dd,
+__global__ void bsk_fourier_kernel(const uint64_t* polys, uint32_t nouts, const double4* tw_dd,
                                    const double4* twist_dd, double2* bskf);
+__global__ void bsk_split_kernel(const uint64_t* bsk, uint64_t* split);
 __global__ void fft_forward_debug_kernel(const int64_t* poly, const double2* tw,
                                          const double2* twist, double2* spec);
 __global__ void fft_backward_debug_kernel(const double2* spec, const double2* tw,

@@ -94,3 +94,34 @@ def test_fft_added_phase_variance(orc):
     # transform, each ~half. A plain-f64 BSK spectrum (TFHE-rs's way) adds
     # 2^96.19 = 0.31; the double-double BSK removes that third of the error.
     assert 0.12 < frac < 0.25, (frac, np.log2(vs))
+
+
+def test_exact_mask_product_mode():
+    """lv_params.exact_mask_product = 1: bit-exact with the oracle's split
+    (H 2^43 + Lo) mask product, decrypts correctly, and the FFT's added
+    phase variance drops to a negligible fraction of the exact noise."""
+    from oracle.oracle import Oracle, default_params as oracle_params
+    op = oracle_params()
+    op.exact_mask_product = 1
+    orc = Oracle(seed=0, params=op)
+    p = L.default_params()
+    p.exact_mask_product = 1
+    c = L.Context(seed=0, params=p)
+    try:
+        lut = np.array(L.eq_lut(9), np.int32)
+        lid = c.lut(lut)
+        tp = orc.test_poly(lut)
+        rows = [orc.encrypt(v, 9300 + v) for v in (0, 7, 15)]
+        ms = np.stack([orc.modswitch(orc.keyswitch(r)) for r in rows])
+        _, glwe = c.debug_blind_rotate(ms, [lid] * len(rows), glwe=True)
+        assert np.array_equal(glwe, orc.blind_rotate_batch(ms, tp, mode=0))
+        vals = [3, 0, 12, 0, 31 - 16]
+        out = c.pbs(c.encrypt(vals), lut)
+        assert list(c.decrypt(out)) == [L.negacyclic_eval(lut, v) for v in vals]
+        r = L.compute("monday", "friday", ctx=c)
+        assert r["distance"] == 3 and r["pbs_total"] == 108
+        frac = orc.fft_phase_error_var(ms[1], orc.test_poly(np.array(L.identity_lut(), np.int32)))
+        frac /= exact_model_var()
+        assert frac < 0.005, frac  # measured 2^85.8 / 2^97.9 = 2.3e-4
+    finally:
+        c.close()
