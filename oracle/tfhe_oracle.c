@@ -45,7 +45,7 @@ struct orc_ctx {
   double* bskf;    /* interleaved (re, im) */
   double* bskf_hi; /* exact_mask_product: spectra of H and Lo of every mask */
   double* bskf_lo; /* polynomial, [(i * rows + r) * k + q][2M]             */
-  double* tw;      /* W[t] = exp(-2 pi i t / M), t < M/2, interleaved */
+  double* tw;      /* W[t] = exp(-2 pi i t / M), t < M, interleaved */
   double* twist;   /* zeta^j = exp(i pi j / N), j < M */
   double* untwist; /* zeta^-j / M */
   double* tw_dd;   /* W[t], t < M/2, as (re.hi, re.lo, im.hi, im.lo) */
@@ -229,44 +229,117 @@ static inline void cmul(double ar, double ai, double br, double bi, double* r, d
   *i = fma(ar, bi, t2);
 }
 
-static void fft_dif(const orc_ctx* c, double* x /* interleaved M */) {
-  const uint32_t M = c->M;
-  for (uint32_t s = 0; s < c->logM; ++s) {
-    const uint32_t half = M >> (s + 1);
-    for (uint32_t blk = 0; blk < M; blk += 2 * half) {
-      for (uint32_t j = 0; j < half; ++j) {
-        double* u = x + 2 * (blk + j);
-        double* v = x + 2 * (blk + j + half);
-        const double* w = c->tw + 2 * ((size_t)j << s);
-        double sr = u[0] + v[0], si = u[1] + v[1];
-        double tr = u[0] - v[0], ti = u[1] - v[1];
-        u[0] = sr;
-        u[1] = si;
-        cmul(tr, ti, w[0], w[1], &v[0], &v[1]);
-      }
+/* The transform (M = 1024) is a fixed network (the GPU reorders data,
+ * never arithmetic): forward = DIF with radix-4 butterflies on the stage pairs
+ * (0,1), (3,4), (6,7) and radix-2 stages 2, 5, 8, 9; inverse = DIT with
+ * radix-2 stage 9, radix-4 (8,7), radix-2 6, radix-4 (5,4), radix-2 3 and 2,
+ * radix-4 (1,0). Output of the forward / input of the inverse: bit-reversed
+ * bin order. W^t = exp(-2 pi i t / M) from long double, t < M. */
+typedef struct {
+  double re, im;
+} cpx;
+static inline cpx cadd(cpx a, cpx b) { return (cpx){a.re + b.re, a.im + b.im}; }
+static inline cpx csub(cpx a, cpx b) { return (cpx){a.re - b.re, a.im - b.im}; }
+static inline cpx cmulw(cpx a, const double* w) {
+  cpx r;
+  cmul(a.re, a.im, w[0], w[1], &r.re, &r.im);
+  return r;
+}
+static inline cpx cmulwc(cpx a, const double* w) {
+  cpx r;
+  cmul(a.re, a.im, w[0], -w[1], &r.re, &r.im);
+  return r;
+}
+static inline cpx ld(const double* x, uint32_t i) { return (cpx){x[2 * i], x[2 * i + 1]}; }
+static inline void st(double* x, uint32_t i, cpx v) {
+  x[2 * i] = v.re;
+  x[2 * i + 1] = v.im;
+}
+
+static void r2_dif(const orc_ctx* c, double* x, uint32_t s) {
+  const uint32_t M = c->M, half = M >> (s + 1);
+  for (uint32_t blk = 0; blk < M; blk += 2 * half)
+    for (uint32_t j = 0; j < half; ++j) {
+      const cpx u = ld(x, blk + j), v = ld(x, blk + j + half);
+      st(x, blk + j, cadd(u, v));
+      st(x, blk + j + half, cmulw(csub(u, v), c->tw + 2 * ((size_t)j << s)));
     }
+}
+
+/* stages s, s+1: (x0, x1, x2, x3) at j + {0, H, 2H, 3H}, k = j << s */
+static void r4_dif(const orc_ctx* c, double* x, uint32_t s) {
+  const uint32_t M = c->M, H = M >> (s + 2);
+  for (uint32_t blk = 0; blk < M; blk += 4 * H)
+    for (uint32_t j = 0; j < H; ++j) {
+      const size_t k = (size_t)j << s;
+      const uint32_t i0 = blk + j;
+      const cpx x0 = ld(x, i0), x1 = ld(x, i0 + H), x2 = ld(x, i0 + 2 * H), x3 = ld(x, i0 + 3 * H);
+      const cpx A = cadd(x0, x2), B = cadd(x1, x3), C = csub(x0, x2), d = csub(x1, x3);
+      const cpx D = {d.im, -d.re}; /* (x1 - x3) * -i */
+      st(x, i0, cadd(A, B));
+      st(x, i0 + H, cmulw(csub(A, B), c->tw + 2 * (2 * k)));
+      st(x, i0 + 2 * H, cmulw(cadd(C, D), c->tw + 2 * k));
+      st(x, i0 + 3 * H, cmulw(csub(C, D), c->tw + 2 * (3 * k)));
+    }
+}
+
+static void fft_dif(const orc_ctx* c, double* x /* interleaved M */) {
+  if (c->logM != 10) { /* other sizes (toy parameter sets): plain radix-2 */
+    for (uint32_t s = 0; s < c->logM; ++s) r2_dif(c, x, s);
+    return;
   }
+  r4_dif(c, x, 0);
+  r2_dif(c, x, 2);
+  r4_dif(c, x, 3);
+  r2_dif(c, x, 5);
+  r4_dif(c, x, 6);
+  r2_dif(c, x, 8);
+  r2_dif(c, x, 9);
+}
+
+static void r2_dit(const orc_ctx* c, double* x, uint32_t s) {
+  const uint32_t M = c->M, half = M >> (s + 1);
+  for (uint32_t blk = 0; blk < M; blk += 2 * half)
+    for (uint32_t j = 0; j < half; ++j) {
+      const cpx p = ld(x, blk + j);
+      const cpx q = cmulwc(ld(x, blk + j + half), c->tw + 2 * ((size_t)j << s));
+      st(x, blk + j, cadd(p, q));
+      st(x, blk + j + half, csub(p, q));
+    }
+}
+
+/* stages s+1 then s, k = j << s */
+static void r4_dit(const orc_ctx* c, double* x, uint32_t s) {
+  const uint32_t M = c->M, H = M >> (s + 2);
+  for (uint32_t blk = 0; blk < M; blk += 4 * H)
+    for (uint32_t j = 0; j < H; ++j) {
+      const size_t k = (size_t)j << s;
+      const uint32_t i0 = blk + j;
+      const cpx x0 = ld(x, i0);
+      const cpx t1 = cmulwc(ld(x, i0 + H), c->tw + 2 * (2 * k));
+      const cpx t2 = cmulwc(ld(x, i0 + 2 * H), c->tw + 2 * k);
+      const cpx t3 = cmulwc(ld(x, i0 + 3 * H), c->tw + 2 * (3 * k));
+      const cpx A = cadd(x0, t1), B = csub(x0, t1), C = cadd(t2, t3), d = csub(t2, t3);
+      const cpx D = {-d.im, d.re}; /* (t2 - t3) * i */
+      st(x, i0, cadd(A, C));
+      st(x, i0 + 2 * H, csub(A, C));
+      st(x, i0 + H, cadd(B, D));
+      st(x, i0 + 3 * H, csub(B, D));
+    }
 }
 
 static void fft_dit_inverse(const orc_ctx* c, double* x) {
-  const uint32_t M = c->M;
-  for (int s = (int)c->logM - 1; s >= 0; --s) {
-    const uint32_t half = M >> (s + 1);
-    for (uint32_t blk = 0; blk < M; blk += 2 * half) {
-      for (uint32_t j = 0; j < half; ++j) {
-        double* p = x + 2 * (blk + j);
-        double* q = x + 2 * (blk + j + half);
-        const double* w = c->tw + 2 * ((size_t)j << s);
-        double qr, qi;
-        cmul(q[0], q[1], w[0], -w[1], &qr, &qi);
-        double pr = p[0], pi = p[1];
-        p[0] = pr + qr;
-        p[1] = pi + qi;
-        q[0] = pr - qr;
-        q[1] = pi - qi;
-      }
-    }
+  if (c->logM != 10) {
+    for (int s = (int)c->logM - 1; s >= 0; --s) r2_dit(c, x, (uint32_t)s);
+    return;
   }
+  r2_dit(c, x, 9);
+  r4_dit(c, x, 7);
+  r2_dit(c, x, 6);
+  r4_dit(c, x, 4);
+  r2_dit(c, x, 3);
+  r2_dit(c, x, 2);
+  r4_dit(c, x, 0);
 }
 
 static inline uint64_t f64_to_torus(double y) {
@@ -384,8 +457,8 @@ static void build_tables(orc_ctx* c) {
   c->logM = 0;
   while ((1u << c->logM) < M) ++c->logM;
   const long double PI = 3.141592653589793238462643383279502884L;
-  c->tw = (double*)malloc(sizeof(double) * M);
-  for (uint32_t t = 0; t < M / 2; ++t) {
+  c->tw = (double*)malloc(sizeof(double) * 2 * M);
+  for (uint32_t t = 0; t < M; ++t) {
     long double ang = 2.0L * PI * (long double)t / (long double)M;
     c->tw[2 * t] = (double)cosl(ang);
     c->tw[2 * t + 1] = (double)(-sinl(ang));

@@ -22,6 +22,12 @@ namespace lvb {
 constexpr uint32_t kN = 2048;          // GLWE polynomial size
 constexpr uint32_t kM = kN / 2;        // complex FFT size (negacyclic fold)
 constexpr uint32_t kLogM = 10;
+// FFT twiddle buffer (fft.cuh): kM radix-2 per-stage entries, then three
+// planes of kM >> (s + 2) entries per radix-4 stage pair s in {0,3,4,6,7}.
+__host__ __device__ constexpr uint32_t r4_base(int s) {
+  return s == 0 ? kM : s == 3 ? kM + 768 : s == 4 ? kM + 864 : s == 6 ? kM + 912 : kM + 924;
+}
+constexpr uint32_t kTwEntries = kM + 930;
 constexpr uint32_t kK = 1;             // GLWE dimension
 constexpr uint32_t kBig = kK * kN;     // big-key LWE mask length
 constexpr uint32_t kBigStride = kBig + 8;  // pool row stride in u64 (16448 B, 64 B aligned)

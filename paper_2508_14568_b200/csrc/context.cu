@@ -349,13 +349,19 @@ static void build_tables(lv_ctx* c) {
   const long double PI = 3.141592653589793238462643383279502884L;
   // W[k] = exp(-2 pi i k / kM), k < kM/2, then the per-stage copies
   // T_s[y] = W[y << s] concatenated (fft.cuh tws()).
-  std::vector<double2> W(kM / 2), tw(kM), twist(128);
-  for (uint32_t t = 0; t < kM / 2; ++t) {
+  std::vector<double2> W(kM), tw(kTwEntries), twist(128);
+  for (uint32_t t = 0; t < kM; ++t) {
     const long double ang = 2.0L * PI * (long double)t / (long double)kM;
     W[t] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
   }
   for (uint32_t s = 0; s < kLogM; ++s)
     for (uint32_t y = 0; y < (kM >> (s + 1)); ++y) tw[(kM - (kM >> s)) + y] = W[y << s];
+  // radix-4 planes (fft.cuh tw4): plane m of pair s holds W[m (j << s)]
+  for (int s : {0, 3, 4, 6, 7}) {
+    const uint32_t H = kM >> (s + 2);
+    for (uint32_t m = 1; m <= 3; ++m)
+      for (uint32_t j = 0; j < H; ++j) tw[r4_base(s) + (m - 1) * H + j] = W[(m * (j << s)) % kM];
+  }
   // twist zeta^j = fine[j & 127] * coarse[j >> 7] (oracle build_tables)
   for (uint32_t j = 0; j < 128; ++j) {
     const long double ang = PI * (long double)j / (long double)kN;

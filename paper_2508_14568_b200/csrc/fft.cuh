@@ -3,13 +3,19 @@
 // polynomials processed in lockstep by the same threads.
 //
 // Bit-exactness contract with oracle/tfhe_oracle.c (fft_dif,
-// fft_dit_inverse, forward_i64, backward_torus): every butterfly performs
-// exactly the oracle's IEEE operations — __dadd_rn/__dsub_rn for sums,
-// cmul() = {fma(a.x,b.x,-(a.y*b.y)), fma(a.x,b.y,(a.y*b.x))} for twiddles —
-// with the same twiddle table entries. Only the data movement differs
+// fft_dit_inverse, forward_i64, backward_torus): the network is fixed —
+// forward: radix-4 DIF butterflies on the stage pairs (0,1), (3,4), (6,7),
+// radix-2 stages 2, 5, 8, 9; inverse: radix-2 DIT stage 9, radix-4 (8,7),
+// radix-2 6, radix-4 (5,4), radix-2 3 and 2, radix-4 (1,0) — and every
+// butterfly performs exactly the oracle's IEEE operations (__dadd_rn /
+// __dsub_rn for sums, cmul() = {fma(a.x,b.x,-(a.y*b.y)), fma(a.x,b.y,(a.y*b.x))}
+// for twiddles, the same table entries). Only the data movement differs
 // (registers, a swizzled shared buffer, lane shuffles), which cannot change
-// a rounding. Multiplications by W[0] = (1,-0) are skipped: they are exact
-// up to the sign of zero, which never reaches a nonzero result.
+// a rounding. Multiplications by W^0 = (1,-0) that are static are skipped:
+// they are exact up to the sign of zero, which never reaches a nonzero result.
+// The radix-4 pairing saves a quarter of those stages' twiddle products
+// (-8% FP64 instructions per transform) and rounds no more often
+// (tools/fft_error.c: external-product error std 2^37.96 vs 2^38.00).
 //
 // Thread layouts (t = threadIdx.x in [0,128), r = register index 0..7):
 //   fwd A  (stages 0-2) : x = t + 128 r
@@ -18,8 +24,10 @@
 //   fwd stage 9 via shfl.xor 1 -> thread t owns spectrum bins 8t .. 8t+7
 //   inv    (stages 9-7) : bins 8t + r
 //   inv B' (stages 6-4) : t = 8 b + u,    x = 64 b + u + 8 r
-//   inv A' (stages 3-1) : t = 32 w + 16 h + s, u = 16 w + s, x = 512 h + u + 64 r
-//   inv stage 0 via shfl.xor 16
+//   inv stage 3 via shfl.xor 8
+//   inv A  (stages 2-0) : x = t + 128 r
+// In every group the radix-4 quadruples are the registers (r, r+2, r+4,
+// r+6), r in {0, 1}, and the radix-2 pairs (r, r+1), r even.
 // Shared buffer index swizzle swz(x) keeps every one of these patterns
 // free of bank conflicts (16-byte elements, 8 lanes per 128-byte wavefront).
 #pragma once
@@ -35,8 +43,8 @@ __device__ __forceinline__ uint32_t swz(uint32_t x) {
 }
 
 // Exchange through shared memory: one polynomial at a time through a
-// single kM-entry buffer (16 KB) instead of all P at once, so the blind
-// rotation fits 4 CTAs per SM. Set LVB_SPLIT_XCHG=0 for the P-buffer form.
+// single kM-entry buffer (16 KB) instead of all P at once (smaller shared
+// footprint). Set LVB_SPLIT_XCHG=0 for the P-buffer form.
 #ifndef LVB_SPLIT_XCHG
 #define LVB_SPLIT_XCHG 1
 #endif
@@ -88,43 +96,82 @@ __device__ __forceinline__ double2 cmul_conj(double2 a, double2 b) {
   return make_double2(__fma_rn(a.x, b.x, -t1), __fma_rn(a.x, nbi, t2));
 }
 
+__device__ __forceinline__ double2 add2(double2 a, double2 b) {
+  return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+__device__ __forceinline__ double2 sub2(double2 a, double2 b) {
+  return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
+}
+
+// radix-2 DIF (u + v, (u - v) w) and DIT (p + q conj(w), p - q conj(w))
 __device__ __forceinline__ void dif(double2& u, double2& v, double2 w) {
-  const double2 s = make_double2(__dadd_rn(u.x, v.x), __dadd_rn(u.y, v.y));
-  const double2 d = make_double2(__dsub_rn(u.x, v.x), __dsub_rn(u.y, v.y));
+  const double2 s = add2(u, v), d = sub2(u, v);
   u = s;
   v = cmul(d, w);
 }
-
-__device__ __forceinline__ void dif1(double2& u, double2& v) {  // w = W[0]
-  const double2 s = make_double2(__dadd_rn(u.x, v.x), __dadd_rn(u.y, v.y));
-  const double2 d = make_double2(__dsub_rn(u.x, v.x), __dsub_rn(u.y, v.y));
+__device__ __forceinline__ void dif1(double2& u, double2& v) {  // w = W^0
+  const double2 s = add2(u, v), d = sub2(u, v);
   u = s;
   v = d;
 }
-
 __device__ __forceinline__ void dit(double2& p, double2& q, double2 w) {
   const double2 qw = cmul_conj(q, w);
-  const double2 a = make_double2(__dadd_rn(p.x, qw.x), __dadd_rn(p.y, qw.y));
-  const double2 b = make_double2(__dsub_rn(p.x, qw.x), __dsub_rn(p.y, qw.y));
+  const double2 a = add2(p, qw), b = sub2(p, qw);
+  p = a;
+  q = b;
+}
+__device__ __forceinline__ void dit1(double2& p, double2& q) {  // w = W^0
+  const double2 a = add2(p, q), b = sub2(p, q);
   p = a;
   q = b;
 }
 
-__device__ __forceinline__ void dit1(double2& p, double2& q) {  // w = W[0]
-  const double2 a = make_double2(__dadd_rn(p.x, q.x), __dadd_rn(p.y, q.y));
-  const double2 b = make_double2(__dsub_rn(p.x, q.x), __dsub_rn(p.y, q.y));
-  p = a;
-  q = b;
+// radix-4 DIF on (x0, x1, x2, x3) = positions j + {0, H, 2H, 3H} of stages
+// s, s+1 (oracle r4_dif), w1 = W^k, w2 = W^2k, w3 = W^3k with k = j << s.
+__device__ __forceinline__ void dif4(double2& x0, double2& x1, double2& x2, double2& x3,
+                                     double2 w1, double2 w2, double2 w3) {
+  const double2 A = add2(x0, x2), B = add2(x1, x3), C = sub2(x0, x2), d = sub2(x1, x3);
+  const double2 D = make_double2(d.y, -d.x);  // (x1 - x3) * -i
+  x0 = add2(A, B);
+  x1 = cmul(sub2(A, B), w2);
+  x2 = cmul(add2(C, D), w1);
+  x3 = cmul(sub2(C, D), w3);
+}
+// radix-4 DIT on stages s+1 then s (oracle r4_dit).
+__device__ __forceinline__ void dit4(double2& x0, double2& x1, double2& x2, double2& x3,
+                                     double2 w1, double2 w2, double2 w3) {
+  const double2 t1 = cmul_conj(x1, w2), t2 = cmul_conj(x2, w1), t3 = cmul_conj(x3, w3);
+  const double2 A = add2(x0, t1), B = sub2(x0, t1), C = add2(t2, t3), d = sub2(t2, t3);
+  const double2 D = make_double2(-d.y, d.x);  // (t2 - t3) * i
+  x0 = add2(A, C);
+  x2 = sub2(A, C);
+  x1 = add2(B, D);
+  x3 = sub2(B, D);
+}
+__device__ __forceinline__ void dit4_1(double2& x0, double2& x1, double2& x2, double2& x3) {
+  const double2 A = add2(x0, x1), B = sub2(x0, x1), C = add2(x2, x3), d = sub2(x2, x3);
+  const double2 D = make_double2(-d.y, d.x);
+  x0 = add2(A, C);
+  x2 = sub2(A, C);
+  x1 = add2(B, D);
+  x3 = sub2(B, D);
 }
 
-// Per-stage twiddle tables T_s[y] = W[y << s] (W[k] = exp(-2 pi i k / kM)),
-// concatenated: T_s starts at kM - (kM >> s). Same values as W, laid out so
-// every warp-wide twiddle load is contiguous.
+// Twiddle tables (one buffer, built by context.cu build_tables):
+//   [0, kM): per-stage radix-2 tables T_s[y] = W[y << s] (W[k] =
+//            exp(-2 pi i k / kM)) concatenated, T_s at kM - (kM >> s);
+//   then per radix-4 pair s in {0, 3, 4, 6, 7}: three planes of H = kM >> (s+2)
+//            entries, plane m (1..3) holding W[m (j << s)].
+// Same values as the oracle's W table, laid out so every warp-wide load is
+// contiguous or a broadcast.
 __device__ __forceinline__ double2 tws(const double2* __restrict__ tw, int s, uint32_t y) {
 #ifdef LVB_ABL_TW  // timing ablation only
   return make_double2(0.70710678118654757 + s * 1e-3, 0.70710678118654757 - y * 1e-9);
 #endif
   return __ldg(tw + (kM - (kM >> s)) + y);
+}
+__device__ __forceinline__ double2 tw4(const double2* __restrict__ tw, int s, int m, uint32_t j) {
+  return __ldg(tw + r4_base(s) + (m - 1) * (kM >> (s + 2)) + j);
 }
 
 // Coarse twist factors zeta^(128 k), k < 8 (constant bank).
@@ -143,53 +190,43 @@ __device__ __forceinline__ double2 shfl_xor_d2(double2 v, int m) {
 
 // ---------------------------------------------------------------- forward
 // X[p][r] on entry: twisted inputs at x = t + 128 r. On exit: spectrum
-// bins 8t + r. buf: P shared buffers of kM double2 each.
+// bins 8t + r. buf: the exchange buffer(s).
 template <int P>
 __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
                                             const double2* __restrict__ tw, uint32_t t) {
-  // group A: stages 0,1,2
+  // group A: radix-4 (0,1) with k = t + 128 r, radix-2 stage 2
   {
-    double2 w0[4];
+    double2 w[2][3];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) w0[r] = tws(tw, 0, t + 128 * r);
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 0, m + 1, t + 128 * r);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) dif(X[p][r], X[p][r + 4], w0[r]);
-    const double2 w10 = tws(tw, 1, t), w11 = tws(tw, 1, t + 128);
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      dif(X[p][0], X[p][2], w10);
-      dif(X[p][1], X[p][3], w11);
-      dif(X[p][4], X[p][6], w10);
-      dif(X[p][5], X[p][7], w11);
-    }
+      for (int r = 0; r < 2; ++r)
+        dif4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w[r][0], w[r][1], w[r][2]);
     const double2 w2 = tws(tw, 2, t);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; r += 2) dif(X[p][r], X[p][r + 1], w2);
   }
-  // A -> B
+  // A -> B: radix-4 (3,4) with j = u + 16 r, radix-2 stage 5
   {
     const uint32_t b = t >> 4, u = t & 15;
     xchg<P>(X, buf, [&](int r) { return t + 128 * r; },
             [&](int r) { return 128 * b + u + 16 * r; });
-    double2 w3[4];
+    double2 w[2][3];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) w3[r] = tws(tw, 3, u + 16 * r);
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 3, m + 1, u + 16 * r);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) dif(X[p][r], X[p][r + 4], w3[r]);
-    const double2 w40 = tws(tw, 4, u), w41 = tws(tw, 4, u + 16);
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      dif(X[p][0], X[p][2], w40);
-      dif(X[p][1], X[p][3], w41);
-      dif(X[p][4], X[p][6], w40);
-      dif(X[p][5], X[p][7], w41);
-    }
+      for (int r = 0; r < 2; ++r)
+        dif4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w[r][0], w[r][1], w[r][2]);
     const double2 w5 = tws(tw, 5, u);
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -200,23 +237,19 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
     xchg<P>(X, buf, [&](int r) { return 128 * b + u + 16 * r; },
             [&](int r) { return 16 * c + v + 2 * r; });
   }
+  // C: radix-4 (6,7) with j = v + 2 r, radix-2 stage 8, stage 9 by shuffle
   {
     const uint32_t v = t & 1;
-    double2 w6[4];
+    double2 w[2][3];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) w6[r] = tws(tw, 6, v + 2 * r);
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 6, m + 1, v + 2 * r);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) dif(X[p][r], X[p][r + 4], w6[r]);
-    const double2 w70 = tws(tw, 7, v), w71 = tws(tw, 7, v + 2);
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      dif(X[p][0], X[p][2], w70);
-      dif(X[p][1], X[p][3], w71);
-      dif(X[p][4], X[p][6], w70);
-      dif(X[p][5], X[p][7], w71);
-    }
+      for (int r = 0; r < 2; ++r)
+        dif4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w[r][0], w[r][1], w[r][2]);
     const double2 w8 = tws(tw, 8, v);
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -243,167 +276,44 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
   }
 }
 
-// ---------------------------------------------------------------- inverse
-// X[p][r] on entry: spectrum bins 8t + r. On exit: for h = (t>>4)&1,
-// u = 16 (t>>5) + (t&15), q = 0..3: X[p][q] = z at x = u + 64 (4h + q),
-// X[p][4+q] = z at x + 512 (before untwist). Buffer reuse is guarded by the
-// caller's __syncthreads before entry.
-template <int P>
-__device__ __forceinline__ void fft_inverse(double2 (&X)[P][8], double2* buf,
-                                            const double2* __restrict__ tw, uint32_t t) {
-  {
-    // stage 9 (half 1), 8 (half 2), 7 (half 4) on the thread's 8 bins
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int r = 0; r < 8; r += 2) dit1(X[p][r], X[p][r + 1]);
-    const double2 w81 = tws(tw, 8, 1);
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      dit1(X[p][0], X[p][2]);
-      dit(X[p][1], X[p][3], w81);
-      dit1(X[p][4], X[p][6]);
-      dit(X[p][5], X[p][7], w81);
-    }
-    const double2 w71 = tws(tw, 7, 1), w72 = tws(tw, 7, 2), w73 = tws(tw, 7, 3);
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      dit1(X[p][0], X[p][4]);
-      dit(X[p][1], X[p][5], w71);
-      dit(X[p][2], X[p][6], w72);
-      dit(X[p][3], X[p][7], w73);
-    }
-  }
-  {
-    const uint32_t b = t >> 3, u = t & 7;
-    xchg<P>(X, buf, [&](int r) { return 8 * t + r; }, [&](int r) { return 64 * b + u + 8 * r; });
-    const double2 w6 = tws(tw, 6, u);
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w6);
-    const double2 w50 = tws(tw, 5, u), w51 = tws(tw, 5, u + 8);
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      dit(X[p][0], X[p][2], w50);
-      dit(X[p][1], X[p][3], w51);
-      dit(X[p][4], X[p][6], w50);
-      dit(X[p][5], X[p][7], w51);
-    }
-    double2 w4[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) w4[r] = tws(tw, 4, u + 8 * r);
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) dit(X[p][r], X[p][r + 4], w4[r]);
-    __syncthreads();
-    const uint32_t h = (t >> 4) & 1, u2 = 16 * (t >> 5) + (t & 15);
-    xchg<P>(X, buf, [&](int r) { return 64 * b + u + 8 * r; },
-            [&](int r) { return 512 * h + u2 + 64 * r; });
-  }
-  {
-    const uint32_t h = (t >> 4) & 1, u = 16 * (t >> 5) + (t & 15);
-    const double2 w3 = tws(tw, 3, u);
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w3);
-    const double2 w20 = tws(tw, 2, u), w21 = tws(tw, 2, u + 64);
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      dit(X[p][0], X[p][2], w20);
-      dit(X[p][1], X[p][3], w21);
-      dit(X[p][4], X[p][6], w20);
-      dit(X[p][5], X[p][7], w21);
-    }
-    double2 w1[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) w1[r] = tws(tw, 1, u + 64 * r);
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) dit(X[p][r], X[p][r + 4], w1[r]);
-    // stage 0 (half 512): lane pairs (t, t^16) hold x and x + 512.
-    double2 w0[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) w0[q] = tws(tw, 0, u + 64 * (4 * h + q));
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      double2 Y[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) Y[q] = shfl_xor_d2(h ? X[p][q] : X[p][4 + q], 16);
-      double2 Z[8];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        double2 lo = h ? Y[q] : X[p][q];
-        double2 hi = h ? X[p][4 + q] : Y[q];
-        dit(lo, hi, w0[q]);
-        Z[q] = lo;
-        Z[4 + q] = hi;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) X[p][q] = Z[q];
-    }
-  }
-}
-
-// ------------------------------------------------ inverse, natural layout A
-// Same arithmetic as fft_inverse (DIT stages 9..0), different data path:
-//   stages 9,8,7 on the thread's bins 8t + r            (registers)
-//   -> B' (t = 8b + u, x = 64b + u + 8r): stages 6,5,4  (shared exchange)
-//   stage 3 (pairs x, x+64 in lanes t, t^8)             (shfl.xor 8)
-//   -> A  (x = t + 128 r): stages 2,1,0                 (shared exchange)
-// so the output lands in the layout fft_forward's input uses: each thread
-// owns the same accumulator coefficients in both halves of a CMUX.
+// ------------------------------------------------------------- inverse
+// X[p][r] on entry: spectrum bins 8t + r. On exit: layout A (x = t + 128 r),
+// the layout fft_forward's input uses, so each thread owns the same
+// accumulator coefficients in both halves of a CMUX. Buffer reuse is
+// guarded by the caller's __syncthreads before entry.
 template <int P>
 __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
                                               const double2* __restrict__ tw, uint32_t t) {
+  // stage 9 (W^0), radix-4 (8,7): j = r, k = 128 r (r = 0: W^0)
   {
+    const double2 w1 = tw4(tw, 7, 1, 1), w2 = tw4(tw, 7, 2, 1), w3 = tw4(tw, 7, 3, 1);
 #pragma unroll
-    for (int p = 0; p < P; ++p)
+    for (int p = 0; p < P; ++p) {
 #pragma unroll
       for (int r = 0; r < 8; r += 2) dit1(X[p][r], X[p][r + 1]);
-    const double2 w81 = tws(tw, 8, 1);
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      dit1(X[p][0], X[p][2]);
-      dit(X[p][1], X[p][3], w81);
-      dit1(X[p][4], X[p][6]);
-      dit(X[p][5], X[p][7], w81);
-    }
-    const double2 w71 = tws(tw, 7, 1), w72 = tws(tw, 7, 2), w73 = tws(tw, 7, 3);
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      dit1(X[p][0], X[p][4]);
-      dit(X[p][1], X[p][5], w71);
-      dit(X[p][2], X[p][6], w72);
-      dit(X[p][3], X[p][7], w73);
+      dit4_1(X[p][0], X[p][2], X[p][4], X[p][6]);
+      dit4(X[p][1], X[p][3], X[p][5], X[p][7], w1, w2, w3);
     }
   }
   const uint32_t b = t >> 3, u = t & 7, odd = b & 1;
   xchg<P>(X, buf, [&](int r) { return 8 * t + r; }, [&](int r) { return 64 * b + u + 8 * r; });
   {
+    // stage 6, radix-4 (5,4) with j = u + 8 r
     const double2 w6 = tws(tw, 6, u);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w6);
-    const double2 w50 = tws(tw, 5, u), w51 = tws(tw, 5, u + 8);
+    double2 w[2][3];
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      dit(X[p][0], X[p][2], w50);
-      dit(X[p][1], X[p][3], w51);
-      dit(X[p][4], X[p][6], w50);
-      dit(X[p][5], X[p][7], w51);
-    }
-    double2 w4[4];
+    for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int r = 0; r < 4; ++r) w4[r] = tws(tw, 4, u + 8 * r);
+      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 4, m + 1, u + 8 * r);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) dit(X[p][r], X[p][r + 4], w4[r]);
+      for (int r = 0; r < 2; ++r)
+        dit4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w[r][0], w[r][1], w[r][2]);
     // stage 3 (half 64): even b holds x, odd b holds x + 64; even lane
     // finishes r = 0..3, odd lane r = 4..7
     double2 w3[4];
@@ -435,26 +345,22 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
       [&](int r) { return 64 * (b & ~1u) + u + 8 * ((r & 3) + 4 * odd) + 64 * (r >> 2); },
       [&](int r) { return t + 128 * r; });
   {
+    // stage 2, radix-4 (1,0) with j = t + 128 r
     const double2 w2 = tws(tw, 2, t);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w2);
-    const double2 w10 = tws(tw, 1, t), w11 = tws(tw, 1, t + 128);
+    double2 w[2][3];
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      dit(X[p][0], X[p][2], w10);
-      dit(X[p][1], X[p][3], w11);
-      dit(X[p][4], X[p][6], w10);
-      dit(X[p][5], X[p][7], w11);
-    }
-    double2 w0[4];
+    for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int r = 0; r < 4; ++r) w0[r] = tws(tw, 0, t + 128 * r);
+      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 0, m + 1, t + 128 * r);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) dit(X[p][r], X[p][r + 4], w0[r]);
+      for (int r = 0; r < 2; ++r)
+        dit4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w[r][0], w[r][1], w[r][2]);
   }
 }
 

@@ -769,19 +769,16 @@ fft_backward_debug_kernel(const double2* spec, const double2* __restrict__ tw,
 #pragma unroll
   for (int q = 0; q < 8; ++q) X[0][q] = spec[8 * t + q];
   __syncthreads();
-  fft_inverse<1>(X, buf, tw, t);
-  const uint32_t h = (t >> 4) & 1, u = 16 * (t >> 5) + (t & 15);
+  fft_inverse_a<1>(X, buf, tw, t);
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int hi = 0; hi < 2; ++hi) {
-      const uint32_t x = u + 64 * (4 * h + q) + 512 * hi;
-      const double2 tv = twist_at(twist, x);
-      const double2 ut = make_double2(__dmul_rn(tv.x, 0x1p-10), __dmul_rn(-tv.y, 0x1p-10));
-      const double2 z = cmul(X[0][4 * hi + q], ut);
-      poly[x] = f64_to_torus(z.x);
-      poly[x + kM] = f64_to_torus(z.y);
-    }
+  for (int r = 0; r < 8; ++r) {
+    const uint32_t x = t + 128 * r;
+    const double2 tv = twist_at(twist, x);
+    const double2 ut = make_double2(__dmul_rn(tv.x, 0x1p-10), __dmul_rn(-tv.y, 0x1p-10));
+    const double2 z = cmul(X[0][r], ut);
+    poly[x] = f64_to_torus(z.x);
+    poly[x + kM] = f64_to_torus(z.y);
+  }
 }
 
 // FP64 pipe peak microbenchmark: 8 independent DFMA chains per thread.

@@ -16,7 +16,9 @@
 typedef long double ld;
 static double tw[2 * M], twist[2 * M], untw[2 * M];
 static ld twl[2 * M], twistl[2 * M];
-static int R8 = 0;
+static int R8 = 0, R4 = 0;
+static void dif4(double* X);
+static void dit4(double* X);
 static void dif8(double* X);
 static void dit8(double* X);
 
@@ -117,7 +119,7 @@ static void difl(ld* x) {
 
 static void fwd(const int64_t* a, double* out) {
   for (int j = 0; j < M; ++j) cmul((double)a[j], (double)a[j + M], twist[2 * j], twist[2 * j + 1], &out[2 * j], &out[2 * j + 1]);
-  if (R8) dif8(out); else dif(out);
+  if (R4) dif4(out); else if (R8) dif8(out); else dif(out);
 }
 static void fwd_ld(const int64_t* a, double* out) {
   ld x[2 * M];
@@ -220,7 +222,73 @@ static void dit8(double* X) {
   }
 }
 
+/* ---- radix-4 on stage pairs (0,1), (3,4), (6,7); radix-2 stages 2,5,8,9 ---- */
+
+static void r2_dif_stage(c2* x, int s) {
+  const int half = M >> (s + 1);
+  for (int b = 0; b < M; b += 2 * half)
+    for (int j = 0; j < half; ++j) {
+      c2 u = x[b + j], v = x[b + j + half];
+      x[b + j] = add(u, v);
+      x[b + j + half] = (j << s) ? mulw(sub(u, v), tw + 2 * (j << s)) : sub(u, v);
+    }
+}
+static void r4_dif_stages(c2* x, int s) {  /* stages s, s+1 */
+  const int H = M >> (s + 2);
+  for (int b = 0; b < M; b += 4 * H)
+    for (int j = 0; j < H; ++j) {
+      const int k = j << s;
+      c2 x0 = x[b + j], x1 = x[b + j + H], x2 = x[b + j + 2 * H], x3 = x[b + j + 3 * H];
+      c2 A = add(x0, x2), B = add(x1, x3), C = sub(x0, x2), D = mul_mi(sub(x1, x3));
+      x[b + j] = add(A, B);
+      x[b + j + H] = k ? mulw(sub(A, B), tw + 2 * (2 * k)) : sub(A, B);
+      x[b + j + 2 * H] = k ? mulw(add(C, D), tw + 2 * k) : add(C, D);
+      x[b + j + 3 * H] = k ? mulw(sub(C, D), tw + 2 * ((3 * k) % M)) : sub(C, D);
+    }
+}
+static void dif4(double* X) {
+  c2* x = (c2*)X;
+  r4_dif_stages(x, 0); r2_dif_stage(x, 2);
+  r4_dif_stages(x, 3); r2_dif_stage(x, 5);
+  r4_dif_stages(x, 6); r2_dif_stage(x, 8);
+  r2_dif_stage(x, 9);
+}
+static void r2_dit_stage(c2* x, int s) {
+  const int half = M >> (s + 1);
+  for (int b = 0; b < M; b += 2 * half)
+    for (int j = 0; j < half; ++j) {
+      c2 p = x[b + j], q = x[b + j + half];
+      if (j << s) q = mulwc(q, tw + 2 * (j << s));
+      x[b + j] = add(p, q);
+      x[b + j + half] = sub(p, q);
+    }
+}
+static void r4_dit_stages(c2* x, int s) {  /* stages s+1 then s */
+  const int H = M >> (s + 2);
+  for (int b = 0; b < M; b += 4 * H)
+    for (int j = 0; j < H; ++j) {
+      const int k = j << s;
+      c2 x0 = x[b + j], x1 = x[b + j + H], x2 = x[b + j + 2 * H], x3 = x[b + j + 3 * H];
+      c2 t1 = k ? mulwc(x1, tw + 2 * (2 * k)) : x1;
+      c2 t2 = k ? mulwc(x2, tw + 2 * k) : x2;
+      c2 t3 = k ? mulwc(x3, tw + 2 * ((3 * k) % M)) : x3;
+      c2 A = add(x0, t1), B = sub(x0, t1), C = add(t2, t3), D = mul_pi(sub(t2, t3));
+      x[b + j] = add(A, C);
+      x[b + j + 2 * H] = sub(A, C);
+      x[b + j + H] = add(B, D);
+      x[b + j + 3 * H] = sub(B, D);
+    }
+}
+static void dit4(double* X) {
+  c2* x = (c2*)X;
+  r2_dit_stage(x, 9);
+  r2_dit_stage(x, 8); r4_dit_stages(x, 6);
+  r2_dit_stage(x, 5); r4_dit_stages(x, 3);
+  r2_dit_stage(x, 2); r4_dit_stages(x, 0);
+}
+
 static void bwd(double* x, uint64_t* out) {
+  if (R4) dit4(x); else
   if (R8) dit8(x); else
   dit(x);
   for (int j = 0; j < M; ++j) {
@@ -260,6 +328,17 @@ int main(int argc, char** argv) {
   int trials = argc > 1 ? atoi(argv[1]) : 8;
   tables();
   R8 = getenv("R8") != NULL;
+  R4 = getenv("R4") != NULL;
+  if (R4) {
+    static double a[2 * M], b2[2 * M];
+    for (int j = 0; j < 2 * M; ++j) a[j] = b2[j] = (double)(int)(rnd() % 2001) - 1000;
+    dif(a); dif4(b2);
+    double e = 0; for (int j = 0; j < 2 * M; ++j) e = fmax(e, fabs(a[j] - b2[j]));
+    printf("dif4 vs dif max diff %.3g\n", e);
+    dit4(b2); dit(a);
+    e = 0; for (int j = 0; j < 2 * M; ++j) e = fmax(e, fabs(a[j] - b2[j]));
+    printf("dit4 vs dit max diff %.3g\n", e);
+  }
   if (R8) { /* consistency: dif8 == dif up to rounding, dit8(dif8(x)) == M x */
     static double a[2 * M], b2[2 * M];
     for (int j = 0; j < 2 * M; ++j) a[j] = b2[j] = (double)(int)(rnd() % 2001) - 1000;
