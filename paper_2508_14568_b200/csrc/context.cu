@@ -155,9 +155,15 @@ static void launch_keyswitch(lv_ctx* c, const LinDesc* d_desc, uint32_t count, u
     const uint32_t mt = (cnt + 127) / 128;
     ks_digits_kernel<<<dim3((kBig + 1 + 255) / 256, mt * 128), 256, 0, c->stream>>>(
         d_desc + off, c->d_pool, kBigStride, cnt, dig, body);
-    ks_mma_kernel<<<dim3(ks_tc_ntiles(c->p.n), mt), 128, ks_tc_smem_bytes(), c->stream>>>(
-        dig, c->d_ksk_bt, c->d_ksk_bias, body, c->p.n, cnt, d_ms + (size_t)off * stride, stride,
-        small_out ? small_out + (size_t)off * row : nullptr);
+    CUtensorMap amap;
+    if (c->ks_tma && make_ks_tensor_map(&amap, dig, (uint64_t)mt * 128, 128))
+      ks_mma_tma_kernel<<<dim3(ks_tc_ntiles(c->p.n), mt), 128, ks_tma_smem_bytes(), c->stream>>>(
+          amap, c->ksk_map, c->d_ksk_bias, body, c->p.n, cnt, d_ms + (size_t)off * stride, stride,
+          small_out ? small_out + (size_t)off * row : nullptr);
+    else
+      ks_mma_kernel<<<dim3(ks_tc_ntiles(c->p.n), mt), 128, ks_tc_smem_bytes(), c->stream>>>(
+          dig, c->d_ksk_bt, c->d_ksk_bias, body, c->p.n, cnt, d_ms + (size_t)off * stride, stride,
+          small_out ? small_out + (size_t)off * row : nullptr);
   }
 #else
   KsArgs ka{d_desc, c->d_pool, kBigStride, c->d_ksk, c->d_ksk_bias, c->p.n, count, d_ms, stride,
@@ -399,6 +405,7 @@ static void keygen(lv_ctx* c) {
     ksk_limbs_kernel<<<dim3((kBig * kKsLevel + 255) / 256, rows / 8), 256, 0, c->stream>>>(
         c->d_ksk, n, c->d_ksk_bt);
     LV_CUDA(cudaGetLastError());
+    c->ks_tma = !std::getenv("LVB_KS_NO_TMA") && make_ks_tensor_map(&c->ksk_map, c->d_ksk_bt, rows, 256);
   }
   uint64_t* d_bsk = nullptr;
   LV_CUDA(cudaMalloc(&d_bsk, (size_t)n * kRows * (kK + 1) * kN * sizeof(uint64_t)));
@@ -529,6 +536,8 @@ int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
                                    (int)blind_rotate_smem_bytes(p.n, true)));
       LV_CUDA(cudaFuncSetAttribute(ks_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)ks_tc_smem_bytes()));
+      LV_CUDA(cudaFuncSetAttribute(ks_mma_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)ks_tma_smem_bytes()));
       LV_CUDA(cudaFuncSetAttribute(blind_rotate_pair_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)blind_rotate_pair_smem_bytes(p.n)));

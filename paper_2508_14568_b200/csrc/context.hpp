@@ -105,6 +105,8 @@ struct lv_ctx {
   lvb::DevBuf<uint64_t> u64a, u64b;
   // tensor-core key switch: KSK byte limbs (transposed, K-major), digits, bodies
   uint8_t* d_ksk_bt = nullptr;
+  CUtensorMap ksk_map;          // TMA view of d_ksk_bt (ks_mma_tma_kernel)
+  bool ks_tma = false;
   lvb::DevBuf<uint8_t> ks_digits;
   lvb::DevBuf<uint64_t> ks_body;
 

@@ -1,6 +1,7 @@
 // Kernel argument structs and launch wrappers (host <-> device contract).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstddef>
@@ -140,5 +141,11 @@ __global__ void ks_mma_kernel(const uint8_t* digits, const uint8_t* bt, const ui
                               const uint64_t* body, uint32_t n, uint32_t count, uint16_t* ms,
                               uint32_t ms_stride, uint64_t* small_out);
 size_t ks_tc_smem_bytes();
+__global__ void ks_mma_tma_kernel(const __grid_constant__ CUtensorMap tm_a,
+                                  const __grid_constant__ CUtensorMap tm_b, const uint64_t* bias,
+                                  const uint64_t* body, uint32_t n, uint32_t count, uint16_t* ms,
+                                  uint32_t ms_stride, uint64_t* small_out);
+size_t ks_tma_smem_bytes();
+bool make_ks_tensor_map(CUtensorMap* map, const uint8_t* base, uint64_t rows, uint32_t box_rows);
 uint32_t ks_tc_ntiles(uint32_t n);
 }  // namespace lvb

@@ -16,6 +16,7 @@
 // (K = 32 each) per block and commits to an mbarrier; the epilogue reads TMEM
 // (tcgen05.ld 32x32b), recombines the limbs and applies bias, body and the
 // modulus switch. Bit-identical to the CUDA-core keyswitch_kernel.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -231,6 +232,177 @@ ks_mma_kernel(const uint8_t* __restrict__ digits, const uint8_t* __restrict__ bt
 }
 
 size_t ks_tc_smem_bytes() { return kTcSmem; }
+
+// ---------------------------------------------------------------- TMA form
+// Same GEMM, operands staged by the Tensor Memory Accelerator: per K block
+// (128 bytes) one 2D box of A (128 item rows) and one of B (256 limb rows)
+// land in shared memory in the 128-byte-swizzled K-major layout the UMMA
+// descriptors read directly (SWIZZLE_128B, 8-row groups 1024 B apart); a
+// 4-stage ring of full/empty mbarriers decouples the producer thread (TMA)
+// from the MMA-issuing thread, so the tensor cores never wait on a CTA-wide
+// barrier. Bit-identical to ks_mma_kernel.
+constexpr uint32_t kTmaStages = 4;
+constexpr uint32_t kTmaStageBytes = kTcSmemA + kTcSmemB;  // 48 KB
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0,
+                                            int32_t c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(128, 1)
+ks_mma_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                  const uint64_t* __restrict__ bias, const uint64_t* __restrict__ body, uint32_t n,
+                  uint32_t count, uint16_t* ms, uint32_t ms_stride, uint64_t* small_out) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[kTmaStages], empty[kTmaStages], done;
+  __shared__ uint32_t taddr_s;
+
+  const uint32_t t = threadIdx.x, warp = t >> 5;
+  const uint32_t m0 = blockIdx.y * kTcM;
+  const uint32_t nt = blockIdx.x;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&taddr_s)),
+                 "r"(kTcN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    for (uint32_t s = 0; s < kTmaStages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&done)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_b)) : "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = taddr_s;
+
+  if (t == 0) {
+    // producer: K block kb into stage kb % S once its previous MMAs committed
+    for (uint32_t kb = 0; kb < kTcNumKB; ++kb) {
+      const uint32_t s = kb % kTmaStages;
+      if (kb >= kTmaStages) mbar_wait(smem_u32(&empty[s]), ((kb / kTmaStages) - 1) & 1);
+      const uint32_t a = smem_u32(smem + s * kTmaStageBytes), b = a + kTcSmemA;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       smem_u32(&full[s])),
+                   "r"(kTmaStageBytes)
+                   : "memory");
+      tma_load_2d(a, &tm_a, (int32_t)(kb * kTcKB), (int32_t)m0, smem_u32(&full[s]));
+      tma_load_2d(b, &tm_b, (int32_t)(kb * kTcKB), (int32_t)(nt * kTcN), smem_u32(&full[s]));
+    }
+  } else if (t == 32) {
+    // MMA issuer: 4 x (K = 32) per block, commit frees the stage
+    const uint32_t idesc =
+        (2u << 4) | (0u << 7) | (0u << 10) | ((kTcN >> 3) << 17) | ((kTcM >> 4) << 24);
+    for (uint32_t kb = 0; kb < kTcNumKB; ++kb) {
+      const uint32_t s = kb % kTmaStages;
+      mbar_wait(smem_u32(&full[s]), (kb / kTmaStages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a = smem_u32(smem + s * kTmaStageBytes), b = a + kTcSmemA;
+#pragma unroll
+      for (uint32_t q = 0; q < kTcKB / 32; ++q) {
+        const uint64_t da = umma_desc_sw128(a + q * 32), db = umma_desc_sw128(b + q * 32);
+        const uint32_t acc = (kb > 0 || q > 0) ? 1u : 0u;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&empty[s]))
+                   : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(&done))
+                 : "memory");
+  }
+  mbar_wait(smem_u32(&done), 0);
+  __syncwarp();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+
+  // epilogue: warp w reads lanes 32w..32w+31 (items), 32 columns at a time
+  const uint32_t item = m0 + t;
+  const uint32_t lane_base = (warp * 32) << 16;
+#pragma unroll 1
+  for (uint32_t ch = 0; ch < kTcN / 32; ++ch) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(tmem + lane_base + ch * 32));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (item < count) {
+#pragma unroll
+      for (uint32_t i = 0; i < 4; ++i) {
+        const uint32_t c = nt * kTcCols + ch * 4 + i;
+        if (c > n) continue;
+        uint64_t s = 0;
+#pragma unroll
+        for (uint32_t b = 0; b < 8; ++b) s += (uint64_t)r[i * 8 + b] << (8 * b);
+        uint64_t v = bias[c] - s;
+        if (c == n) v += body[item];
+        if (small_out) small_out[(size_t)item * (n + 1) + c] = v;
+        ms[(size_t)item * ms_stride + c] = (uint16_t)modswitch(v);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcN));
+}
+
+size_t ks_tma_smem_bytes() { return kTmaStages * kTmaStageBytes + 1024; }
+
+// Host: 2D tensor maps (K bytes innermost, rows), 128 x rows boxes,
+// 128-byte swizzle. cuTensorMapEncodeTiled through the runtime's driver
+// entry point (no libcuda link dependency).
+bool make_ks_tensor_map(CUtensorMap* map, const uint8_t* base, uint64_t rows, uint32_t box_rows) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  const cuuint64_t dims[2] = {kKsK, rows};
+  const cuuint64_t strides[1] = {kKsK};
+  const cuuint32_t box[2] = {kTcKB, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides,
+                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 uint32_t ks_tc_ntiles(uint32_t n) { return (n + 1 + kTcCols - 1) / kTcCols; }
 
 }  // namespace lvb
