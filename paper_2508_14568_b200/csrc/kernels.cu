@@ -36,6 +36,26 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
 }
 
 // ------------------------------------------------------------------ BR
+// Output of one sample-extracted coefficient j (value v = a'_j or b') to
+// the item's BrOut: mode 0 writes the LWE (+ body_add * Delta on the body);
+// mode 1 is the fused cell epilogue (kernel.cpp:152-163): v = step, and
+// dv' = step - dh, dh' = step - dv in place (+ score-path snapshots).
+__device__ __forceinline__ void br_output(const BrOut& o, uint64_t* pool, uint32_t S, uint32_t j,
+                                          uint64_t v) {
+  if (o.mode == 0) {
+    pool[(size_t)o.slot_a * S + j] = j == kN ? v + (uint64_t)(int64_t)o.body_add * kDelta : v;
+    return;
+  }
+  uint64_t* dv = pool + (size_t)o.slot_a * S;
+  uint64_t* dh = pool + (size_t)o.slot_b * S;
+  const uint64_t v_in = dv[j], h_in = dh[j];
+  const uint64_t v_out = v - h_in, h_out = v - v_in;
+  dv[j] = v_out;
+  dh[j] = h_out;
+  if (o.snap_dv != kNoSlot) pool[(size_t)o.snap_dv * S + j] = v_out;
+  if (o.snap_dh != kNoSlot) pool[(size_t)o.snap_dh * S + j] = h_out;
+}
+
 // o = d0 * b0 + d1 * b1 for one spectrum bin, in the MAC's fixed FMA order
 // (oracle mac_bins): row 0 then row 1, real part first.
 __device__ __forceinline__ double2 mac2(double2 d0, double2 b0, double2 d1, double2 b1) {
@@ -207,29 +227,9 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
 
   // sample extract coefficient 0 (a'_0 = A_0, a'_j = -A_{N-j}, b' = B_0) + epilogue
   const BrOut o = a.outs[item];
-  const uint32_t S = a.pool_stride;
-  if (o.mode == 0) {
-    uint64_t* out = a.pool + (size_t)o.slot_a * S;
-    for (uint32_t j = t; j <= kN; j += 128) {
-      uint64_t v = j == 0 ? acc[0] : (j == kN ? acc[kN] + (uint64_t)(int64_t)o.body_add * kDelta
-                                              : (uint64_t)0 - acc[kN - j]);
-      out[j] = v;
-    }
-  } else {
-    uint64_t* dv = a.pool + (size_t)o.slot_a * S;
-    uint64_t* dh = a.pool + (size_t)o.slot_b * S;
-    uint64_t* sdv = o.snap_dv == kNoSlot ? nullptr : a.pool + (size_t)o.snap_dv * S;
-    uint64_t* sdh = o.snap_dh == kNoSlot ? nullptr : a.pool + (size_t)o.snap_dh * S;
-    for (uint32_t j = t; j <= kN; j += 128) {
-      const uint64_t step = j == 0 ? acc[0] : (j == kN ? acc[kN] : (uint64_t)0 - acc[kN - j]);
-      const uint64_t v_in = dv[j], h_in = dh[j];
-      const uint64_t v_out = step - h_in, h_out = step - v_in;
-      dv[j] = v_out;
-      dh[j] = h_out;
-      if (sdv) sdv[j] = v_out;
-      if (sdh) sdh[j] = h_out;
-    }
-  }
+  for (uint32_t j = t; j <= kN; j += 128)
+    br_output(o, a.pool, a.pool_stride, j,
+              j == 0 ? acc[0] : (j == kN ? acc[kN] : (uint64_t)0 - acc[kN - j]));
 }
 __global__ void __launch_bounds__(128, 3) blind_rotate_kernel(BrArgs a) {
   blind_rotate_body<false>(a);
@@ -376,29 +376,9 @@ blind_rotate_pair_kernel(BrArgs a) {
 
   // sample extract: the mask CTA writes a' (j < kN), the body CTA b' (j = kN)
   const BrOut o = a.outs[item];
-  const uint32_t S = a.pool_stride;
   const uint32_t j0 = p == 0 ? t : kN + t, j1 = p == 0 ? kN : kN + 1;
-  if (o.mode == 0) {
-    uint64_t* out = a.pool + (size_t)o.slot_a * S;
-    for (uint32_t j = j0; j < j1; j += 128)
-      out[j] = j == 0 ? acc[0]
-                      : (j == kN ? acc[0] + (uint64_t)(int64_t)o.body_add * kDelta
-                                 : (uint64_t)0 - acc[kN - j]);
-  } else {
-    uint64_t* dv = a.pool + (size_t)o.slot_a * S;
-    uint64_t* dh = a.pool + (size_t)o.slot_b * S;
-    uint64_t* sdv = o.snap_dv == kNoSlot ? nullptr : a.pool + (size_t)o.snap_dv * S;
-    uint64_t* sdh = o.snap_dh == kNoSlot ? nullptr : a.pool + (size_t)o.snap_dh * S;
-    for (uint32_t j = j0; j < j1; j += 128) {
-      const uint64_t step = j == 0 ? acc[0] : (j == kN ? acc[0] : (uint64_t)0 - acc[kN - j]);
-      const uint64_t v_in = dv[j], h_in = dh[j];
-      const uint64_t v_out = step - h_in, h_out = step - v_in;
-      dv[j] = v_out;
-      dh[j] = h_out;
-      if (sdv) sdv[j] = v_out;
-      if (sdh) sdh[j] = h_out;
-    }
-  }
+  for (uint32_t j = j0; j < j1; j += 128)
+    br_output(o, a.pool, a.pool_stride, j, j == 0 || j == kN ? acc[0] : (uint64_t)0 - acc[kN - j]);
 }
 
 // acc (16 KB) + exchange buffer (16 KB) + 2 published spectra (32 KB) + ms.
