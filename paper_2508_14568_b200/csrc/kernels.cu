@@ -231,7 +231,10 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
     br_output(o, a.pool, a.pool_stride, j,
               j == 0 ? acc[0] : (j == kN ? acc[kN] : (uint64_t)0 - acc[kN - j]));
 }
-__global__ void __launch_bounds__(128, 3) blind_rotate_kernel(BrArgs a) {
+#ifndef LVB_BR_CTAS
+#define LVB_BR_CTAS 3  // resident CTAs per SM the register allocation targets
+#endif
+__global__ void __launch_bounds__(128, LVB_BR_CTAS) blind_rotate_kernel(BrArgs a) {
   blind_rotate_body<false>(a);
 }
 __global__ void __launch_bounds__(128, 2) blind_rotate_exact_kernel(BrArgs a) {
