@@ -265,8 +265,21 @@ blind_rotate_pair_kernel(BrArgs a) {
   uint16_t* ms = reinterpret_cast<uint16_t*>(smem + kN * 8 + 3 * kM * 16);
   cg::cluster_group cluster = cg::this_cluster();
   const uint32_t p = cluster.block_rank();
-  double2* pspec = cluster.map_shared_rank(spec, p ^ 1u);  // the partner's inbox
+  __shared__ __align__(8) uint64_t inbox_full[2];  // my inbox buffers' arrival barriers
   const uint32_t t = threadIdx.x;
+  // shared::cluster addresses of the partner's inbox and its barriers
+  uint32_t r_inbox, r_full;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(r_inbox) : "r"((uint32_t)__cvta_generic_to_shared(spec)), "r"(p ^ 1u));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(r_full) : "r"((uint32_t)__cvta_generic_to_shared(inbox_full)), "r"(p ^ 1u));
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&inbox_full[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&inbox_full[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
   const uint32_t item = blockIdx.x >> 1;
   const uint32_t n = a.n;
 
@@ -297,11 +310,14 @@ blind_rotate_pair_kernel(BrArgs a) {
   }
   cluster.sync();  // the partner's shared memory is live before any DSMEM access
 
-  // The inbox alternates between two buffers by executed-CMUX parity, so the
-  // one cluster barrier per CMUX (after delivering) also guarantees the
-  // partner finished reading the buffer being overwritten (it read it two
-  // CMUXes ago, before arriving at the last barrier).
-  uint32_t parity = 0;
+  // Spectra travel by st.async into the partner's inbox, each store
+  // completing bytes on the partner's inbox barrier; the receiver arms its
+  // barrier (expect 16 KB) and waits with cluster-scope acquire. No cluster
+  // barrier per CMUX: the inbox alternates between two buffers by
+  // executed-CMUX parity, and a CTA overwrites a buffer only after receiving
+  // the partner's next spectrum, which the partner sends after finishing its
+  // MAC on that buffer.
+  uint32_t parity = 0, uses = 0;
   for (uint32_t i = 0; i < n; ++i) {
     __syncthreads();  // previous update of acc visible to the rotated reads
     const uint32_t rot = ms[i];
@@ -333,12 +349,32 @@ blind_rotate_pair_kernel(BrArgs a) {
       X[0][r] = cmul(make_double2((double)d[0], (double)d[1]), tz[r]);
     }
     fft_forward<1>(X, buf, tw, t);
-    // push the spectrum into the partner's inbox (remote stores, no latency
-    // on this side); the barrier's release/acquire makes them visible
-    double2* theirs = pspec + parity * kM;
+    const uint32_t my_full = (uint32_t)__cvta_generic_to_shared(&inbox_full[parity]);
+    if (t == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(my_full),
+                   "r"(kM * 16u)
+                   : "memory");
+    {
+      const uint32_t dst = r_inbox + parity * kM * 16u + t * 16u;
+      const uint32_t bar = r_full + parity * 8u;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) theirs[q * 128 + t] = X[0][q];
-    cluster.sync();  // both spectra delivered
+      for (int q = 0; q < 8; ++q)
+        asm volatile(
+            "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+                dst + q * 128u * 16u),
+            "d"(X[0][q].x), "d"(X[0][q].y), "r"(bar)
+            : "memory");
+    }
+    {
+      const uint32_t ph = uses & 1u;
+      asm volatile(
+          "{\n\t.reg .pred P1;\n\t"
+          "WAIT_INBOX:\n\t"
+          "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+          "@!P1 bra WAIT_INBOX;\n\t}" ::"r"(my_full),
+          "r"(ph)
+          : "memory");
+    }
     {
       const double2* other_spec = spec + parity * kM;
 #pragma unroll
@@ -357,6 +393,7 @@ blind_rotate_pair_kernel(BrArgs a) {
         X[0][q] = o;
       }
     }
+    uses += parity;  // each buffer's barrier completes once per two CMUXes
     parity ^= 1u;
     __syncthreads();  // forward's last buffer reads precede the inverse's writes
     fft_inverse_a<1>(X, buf, tw, t);  // its barriers also order the rotated reads before the update
