@@ -347,16 +347,19 @@ class Context:
         _check(lib().lv_lut_upload(self._h, _ptr(e, ctypes.c_int32), ctypes.byref(out)))
         return out.value
 
-    def pbs(self, cts, lut):
-        """Backend::pbs over a batch; ``lut`` is a Lut16 (entries) or an id array."""
+    def pbs(self, cts, lut=None, lut_ids=None):
+        """Backend::pbs over a batch: ``lut`` is one Lut16 (16 entries) or one
+        registered id (``ctx.lut``) applied to every ciphertext; ``lut_ids``
+        gives one registered id per ciphertext instead."""
         c = _u32(cts)
-        la = np.asarray(lut)
-        if la.size == 16:
-            ids = np.full(c.size, self.lut(la), np.uint32)
-        elif la.ndim == 0:
-            ids = np.full(c.size, int(la), np.uint32)
+        if lut_ids is not None:
+            ids = _u32(lut_ids)
+        elif lut is not None and np.ndim(lut) == 0:
+            ids = np.full(c.size, int(lut), np.uint32)
+        elif lut is not None:
+            ids = np.full(c.size, self.lut(lut), np.uint32)
         else:
-            ids = _u32(la)
+            raise InvalidParams("pbs needs a Lut16, a lut id or per-ciphertext lut_ids")
         if ids.size != c.size:
             raise InvalidParams("one lut id per ciphertext")
         out = np.zeros(c.size, np.uint32)
