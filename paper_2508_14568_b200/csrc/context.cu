@@ -517,6 +517,8 @@ int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
         p.ks_base_log != kKsBaseLog || p.ks_level != kKsLevel)
       throw Error(LV_ERR_INVALID_PARAMS, "parameter set does not match the compiled kernels");
     if (p.n < 1 || p.n > 4096) throw Error(LV_ERR_INVALID_PARAMS, "n out of range");
+    if (p.exact_mask_product > 1)
+      throw Error(LV_ERR_INVALID_PARAMS, "exact_mask_product must be 0 or 1");
     if (p.max_variance_budget < 1.0)  // backend.hpp:85-88
       throw Error(LV_ERR_INVALID_PARAMS, "noise budget must be at least 1");
     int ndev = 0;
