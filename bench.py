@@ -166,6 +166,21 @@ def traffic_from_profile():
     return None
 
 
+def pipes_from_profile():
+    """FP64 / L1 pipe utilisation of the committed ncu capture of the same
+    kernel (profiles/r01_br_full.json): the instruction-level view of the
+    bound beside the algorithmic-FLOP fraction."""
+    p = os.path.join(ROOT, "profiles", "r01_br_full.json")
+    try:
+        d = json.load(open(p))["launches"][0]
+        pct = lambda k: float(d[k].split()[0]) / 100.0  # noqa: E731
+        return {"fp64_pipe_active": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                "l1tex_throughput": pct("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                "source": "profiles/r01_br_full.json (ncu --set full)"}
+    except Exception:
+        return None
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return 0
@@ -329,6 +344,7 @@ def main():
         "kernel_ms": {"blind_rotate": br_ms, "keyswitch": ks_ms},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic_from_profile(),
+                     "ncu_pipes": pipes_from_profile(),
                      "kernel": "blind_rotate_kernel",
                      "note": "209 MFLOP/PBS algorithmic (5(N/2)log2(N/2) per transform + MAC); "
                              "peak = DFMA throughput measured on this GPU by lv_bench_fp64_peak "
