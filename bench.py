@@ -354,7 +354,12 @@ def main():
         "e2e": {"value": ws * BATCH / e2e_s, "unit": "PBS/s",
                 "h2d_bytes_per_step": int(rows.nbytes), "d2h_bytes_per_step": int(rows.nbytes),
                 "correct": bool(e2e_ok)},
-        "gpu_launches": 3 * args.steps,  # per step: ks_digits, ks_mma (tcgen05), blind_rotate
+        # per timed step: ks_digits, ks_mma_tma (tcgen05), blind_rotate; plus
+        # one L2-flush kernel between steps, outside the event-timed span
+        "gpu_launches": 3 * args.steps,
+        "gpu_launches_detail": {"per_step": ["ks_digits_kernel", "ks_mma_tma_kernel",
+                                             "blind_rotate_kernel"],
+                                "l2_flush_between_steps": args.steps},
         "clocks": clocks,
     }
     if rank == 0 and ws == 1 and not args.no_extras:  # extras and CPU baseline at N=1 only
