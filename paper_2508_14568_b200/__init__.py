@@ -475,14 +475,15 @@ def fp64_peak_tflops() -> float:
 
 from .leuven import (  # noqa: E402  (reference-shaped pipeline API)
     AlphabetSpec, BandSpec, DistanceRun, EqTable, EncryptedString, band_cell_count, build_eq_table,
-    compute, compute_batch, distance_encrypted, distance_preprocessed, distance_preprocessed_batch,
+    compute, compute_batch, distance_batch, distance_encrypted, distance_preprocessed,
+    distance_preprocessed_batch,
     encrypt_string, load_eq_table, plan_trace, report_json, run_batch, save_eq_table, wf_distance,
 )
 
 __all__ = [
     "Context", "Params", "default_params", "negacyclic_eval", "identity_lut", "eq_lut", "AlphabetSpec",
     "BandSpec", "DistanceRun", "EqTable", "EncryptedString", "band_cell_count", "build_eq_table",
-    "compute", "compute_batch", "distance_encrypted", "distance_preprocessed",
+    "compute", "compute_batch", "distance_batch", "distance_encrypted", "distance_preprocessed",
     "distance_preprocessed_batch", "encrypt_string", "plan_trace", "wf_distance", "run_batch",
     "report_json", "save_eq_table", "load_eq_table", "Error", "OutOfRangeValue", "NoiseBudgetExceeded",
     "ValueOutsideLutHalf", "PackingViolation", "CharNotInAlphabet", "CharNotInSubset",
