@@ -105,6 +105,46 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+// Epilogue shared by both GEMM forms: warp w reads TMEM lanes 32w..32w+31
+// (its items), 32 columns (4 output coefficients x 8 limbs) at a time,
+// recombines the limbs mod 2^64, repays the +4 digit bias, adds the body
+// and stores the modulus-switched coefficient.
+__device__ __forceinline__ void ks_epilogue(uint32_t tmem, uint32_t warp, uint32_t item,
+                                            uint32_t nt, const uint64_t* __restrict__ bias,
+                                            const uint64_t* __restrict__ body, uint32_t n,
+                                            uint32_t count, uint16_t* ms, uint32_t ms_stride,
+                                            uint64_t* small_out) {
+  const uint32_t lane_base = (warp * 32) << 16;
+#pragma unroll 1
+  for (uint32_t ch = 0; ch < kTcN / 32; ++ch) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(tmem + lane_base + ch * 32));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (item < count) {
+#pragma unroll
+      for (uint32_t i = 0; i < 4; ++i) {
+        const uint32_t c = nt * kTcCols + ch * 4 + i;
+        if (c > n) continue;
+        uint64_t s = 0;
+#pragma unroll
+        for (uint32_t b = 0; b < 8; ++b) s += (uint64_t)r[i * 8 + b] << (8 * b);
+        uint64_t v = bias[c] - s;
+        if (c == n) v += body[item];
+        if (small_out) small_out[(size_t)item * (n + 1) + c] = v;
+        ms[(size_t)item * ms_stride + c] = (uint16_t)modswitch(v);
+      }
+    }
+  }
+}
+
 constexpr size_t kTcSmemA = kTcM * kTcKB;  // 16 KB
 constexpr size_t kTcSmemB = kTcN * kTcKB;  // 32 KB
 constexpr size_t kTcSmem = 2 * (kTcSmemA + kTcSmemB) + 1024;
@@ -194,37 +234,7 @@ ks_mma_kernel(const uint8_t* __restrict__ digits, const uint8_t* __restrict__ bt
   mbar_wait(smem_u32(&mbar[(kTcNumKB - 1) & 1]), ((kTcNumKB - 1) >> 1) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;");
 
-  // epilogue: warp w reads lanes 32w..32w+31 (items), 32 columns at a time
-  const uint32_t item = m0 + t;
-  const uint32_t lane_base = (warp * 32) << 16;
-#pragma unroll 1
-  for (uint32_t ch = 0; ch < kTcN / 32; ++ch) {
-    uint32_t r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(tmem + lane_base + ch * 32));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (item < count) {
-#pragma unroll
-      for (uint32_t i = 0; i < 4; ++i) {
-        const uint32_t c = nt * kTcCols + ch * 4 + i;
-        if (c > n) continue;
-        uint64_t s = 0;
-#pragma unroll
-        for (uint32_t b = 0; b < 8; ++b) s += (uint64_t)r[i * 8 + b] << (8 * b);
-        uint64_t v = bias[c] - s;
-        if (c == n) v += body[item];
-        if (small_out) small_out[(size_t)item * (n + 1) + c] = v;
-        ms[(size_t)item * ms_stride + c] = (uint16_t)modswitch(v);
-      }
-    }
-  }
+  ks_epilogue(tmem, warp, m0 + t, nt, bias, body, n, count, ms, ms_stride, small_out);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0)
@@ -336,37 +346,7 @@ ks_mma_tma_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constan
   __syncwarp();
   asm volatile("tcgen05.fence::after_thread_sync;");
 
-  // epilogue: warp w reads lanes 32w..32w+31 (items), 32 columns at a time
-  const uint32_t item = m0 + t;
-  const uint32_t lane_base = (warp * 32) << 16;
-#pragma unroll 1
-  for (uint32_t ch = 0; ch < kTcN / 32; ++ch) {
-    uint32_t r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(tmem + lane_base + ch * 32));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (item < count) {
-#pragma unroll
-      for (uint32_t i = 0; i < 4; ++i) {
-        const uint32_t c = nt * kTcCols + ch * 4 + i;
-        if (c > n) continue;
-        uint64_t s = 0;
-#pragma unroll
-        for (uint32_t b = 0; b < 8; ++b) s += (uint64_t)r[i * 8 + b] << (8 * b);
-        uint64_t v = bias[c] - s;
-        if (c == n) v += body[item];
-        if (small_out) small_out[(size_t)item * (n + 1) + c] = v;
-        ms[(size_t)item * ms_stride + c] = (uint16_t)modswitch(v);
-      }
-    }
-  }
+  ks_epilogue(tmem, warp, m0 + t, nt, bias, body, n, count, ms, ms_stride, small_out);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0)
