@@ -19,9 +19,15 @@
  *   for BIT-EXACT ciphertexts (every rounding is an explicit fma / mul /
  *   add that both CPU and GPU round identically).
  *
+ *   The FFT network (radix-4/radix-2 stages, fft_dif / fft_dit_inverse),
+ *   the double-double BSK spectrum computed at keygen, and the optional
+ *   exact-mask-product split (orc_params.exact_mask_product) are part of
+ *   that specification and mirrored by the GPU kernels.
+ *
  *   A second blind-rotation mode multiplies polynomials exactly in
  *   Z_{2^64}[X]/(X^N+1) (schoolbook), independent of any FFT, so the FFT
- *   path's extra phase noise can be measured against an exact product.
+ *   path's extra phase noise can be measured against an exact product
+ *   (orc_fft_phase_error_var accounts it deterministically).
  *
  * Parity anchors (decrypted-value level): the reference's own tests and
  * the compiled reference SimBackend (oracle/_ref, tests/golden/).
