@@ -769,7 +769,8 @@ static void external_product_fft(const orc_ctx* c, size_t i, const uint64_t* glw
       uint64_t* hi = (uint64_t*)malloc(sizeof(uint64_t) * N);
       for (int part = 0; part < 2; ++part) {
         memset(acc, 0, sizeof(double) * 2 * M);
-        for (uint32_t r = 0; r < rows; ++r) {
+        for (uint32_t rr = 0; rr < rows; ++rr) {
+          const uint32_t r = (rr + o) % rows; /* output o: row o first */
           const double* d = specs + (size_t)r * 2 * M;
           const double* b = (part == 0 ? c->bskf_hi : c->bskf_lo) + ((i * rows + r) * k + o) * 2 * M;
           mac_bins(acc, d, b, M);
@@ -781,7 +782,8 @@ static void external_product_fft(const orc_ctx* c, size_t i, const uint64_t* glw
       continue;
     }
     memset(acc, 0, sizeof(double) * 2 * M);
-    for (uint32_t r = 0; r < rows; ++r) {
+    for (uint32_t rr = 0; rr < rows; ++rr) {
+      const uint32_t r = (rr + o) % rows; /* output o: row o first */
       const double* d = specs + (size_t)r * 2 * M;
       const double* b = c->bskf + ((i * rows + r) * (k + 1) + o) * 2 * M;
       for (uint32_t f = 0; f < M; ++f) {

@@ -57,7 +57,8 @@ __device__ __forceinline__ void br_output(const BrOut& o, uint64_t* pool, uint32
 }
 
 // o = d0 * b0 + d1 * b1 for one spectrum bin, in the MAC's fixed FMA order
-// (oracle mac_bins): row 0 then row 1, real part first.
+// (oracle mac_bins): the first pair first, real part first. Output o takes
+// row o first (rows rotated), so each polynomial's own term leads.
 __device__ __forceinline__ double2 mac2(double2 d0, double2 b0, double2 d1, double2 b1) {
   double2 o;
   o.x = __fma_rn(d0.x, b0.x, 0.0);
@@ -169,7 +170,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         const double2 h1 = ld_stream(bq + 384), l1 = ld_stream(bq + 512), b1 = ld_stream(bq + 640);
         Z[0][q] = mac2(d0, h0, d1, h1);
         Z[1][q] = mac2(d0, l0, d1, l1);
-        Z[2][q] = mac2(d0, b0, d1, b1);
+        Z[2][q] = mac2(d1, b1, d0, b0);  // body output: row 1 first
       }
       __syncthreads();  // forward's last buffer reads precede the inverse's writes
       fft_inverse_a<3>(Z, buf, tw, t);
@@ -198,7 +199,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         const double2 b00 = ld_stream(bq), b01 = ld_stream(bq + 128);
         const double2 b10 = ld_stream(bq + 256), b11 = ld_stream(bq + 384);
         X[0][q] = mac2(d0, b00, d1, b10);
-        X[1][q] = mac2(d0, b01, d1, b11);
+        X[1][q] = mac2(d1, b11, d0, b01);  // output o: row o first
       }
       __syncthreads();  // forward's last buffer reads precede the inverse's writes
       fft_inverse_a<2>(X, buf, tw, t);
@@ -379,18 +380,9 @@ blind_rotate_pair_kernel(BrArgs a) {
       const double2* other_spec = spec + parity * kM;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const double2 other = other_spec[q * 128 + t];
-        const double2 d0 = p == 0 ? X[0][q] : other, d1 = p == 0 ? other : X[0][q];
-        double2 o;
-        o.x = __fma_rn(d0.x, b0[q].x, 0.0);
-        o.x = __fma_rn(-d0.y, b0[q].y, o.x);
-        o.y = __fma_rn(d0.x, b0[q].y, 0.0);
-        o.y = __fma_rn(d0.y, b0[q].x, o.y);
-        o.x = __fma_rn(d1.x, b1[q].x, o.x);
-        o.x = __fma_rn(-d1.y, b1[q].y, o.x);
-        o.y = __fma_rn(d1.x, b1[q].y, o.y);
-        o.y = __fma_rn(d1.y, b1[q].x, o.y);
-        X[0][q] = o;
+        // output p = own spectrum x B[row p][out p] + partner's x B[row 1-p][out p]
+        X[0][q] = mac2(X[0][q], p == 0 ? b0[q] : b1[q], other_spec[q * 128 + t],
+                       p == 0 ? b1[q] : b0[q]);
       }
     }
     uses += parity;  // each buffer's barrier completes once per two CMUXes
