@@ -368,7 +368,7 @@ def main():
         except Exception as e:  # reported, never silently dropped
             line["dp_cells"] = {"error": repr(e)}
         try:
-            sample = min(4096, 48 * (os.cpu_count() or 1))
+            sample = min(4096, 64 * (os.cpu_count() or 1))  # ~10 s of host work
             r, cores, dt, ok = cpu_oracle_pbs_rate(sample)
             line["cpu_baseline"] = {"value": r, "unit": "PBS/s", "cores": cores, "kind": "port",
                                     "sample": f"{sample} of the 4096 cfg2 PBS on {cores} threads "
