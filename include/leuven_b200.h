@@ -100,6 +100,18 @@ void lv_ctx_destroy(lv_ctx* ctx);
 const char* lv_last_error(void);
 int lv_abi_version(void);
 
+/* The product's own lookup tables (the ones it bootstraps with), for the
+ * CLI `table` dump / pybind lut_dump (cli.cpp:212-228, module.cpp:97-106):
+ * build_min_lut (kernel.cpp:64-72) in both key encodings and eq_lut(1|9)
+ * (equality.cpp:31-36). */
+typedef enum {
+  LV_TABLE_MINLUT_ORIGINAL = 0,
+  LV_TABLE_MINLUT_NEGATED = 1,
+  LV_TABLE_EQLUT = 2,
+  LV_TABLE_EQLUT9 = 3
+} lv_table;
+int lv_lut_table(int32_t which, int32_t* out16);
+
 /* ---- Backend (backend.hpp:54-76) ---------------------------------------- */
 int lv_encrypt(lv_ctx* ctx, const int32_t* values, size_t count, lv_ct* out);   /* encrypt :54 */
 int lv_trivial(lv_ctx* ctx, const int32_t* values, size_t count, lv_ct* out);   /* trivial :55 */

@@ -205,6 +205,20 @@ int ref_banded_distance(const char* a, const char* b, uint64_t hw, int32_t* out)
 
 uint64_t ref_band_cell_count(uint64_t m, uint64_t ell) { return kernel::band_cell_count(m, ell); }
 
+int ref_eq_cost(const char* technique, int32_t bits, int32_t* out) {
+  try {
+    const std::string t(technique);
+    const equality::EqTechnique tech = t == "standard_2bit" ? equality::EqTechnique::standard_2bit
+                                       : t == "ours_4bit"   ? equality::EqTechnique::ours_4bit
+                                                            : equality::EqTechnique::combined;
+    *out = equality::eq_cost(tech, bits);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return classify(e);
+  }
+}
+
 // cfg2 on the simulated backend: `count` fresh encryptions through
 // SimBackend::pbs with the identity table, `threads` workers each with its
 // own backend (the reference's batch model, cli.cpp:194-207). Returns the

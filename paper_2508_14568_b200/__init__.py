@@ -112,7 +112,7 @@ class Run(ctypes.Structure):
 # Every exported symbol declared in include/leuven_b200.h (checked by tests).
 EXPORTS = [
     "lv_default_params", "lv_ctx_create", "lv_ctx_destroy", "lv_last_error", "lv_abi_version",
-    "lv_encrypt", "lv_trivial", "lv_decrypt", "lv_add", "lv_sub", "lv_scalar_mul",
+    "lv_lut_table", "lv_encrypt", "lv_trivial", "lv_decrypt", "lv_add", "lv_sub", "lv_scalar_mul",
     "lv_scalar_add", "lv_lut_upload", "lv_pbs_batch", "lv_refresh_batch", "lv_predict_variance",
     "lv_get_stats", "lv_get_params", "lv_release", "lv_ledger_variance", "lv_export",
     "lv_import", "lv_phase", "lv_pbs_batch_host", "lv_band_resolve", "lv_edit_distance_ee",
@@ -148,6 +148,7 @@ def lib():
             "lv_ctx_destroy": (None, [vp]),
             "lv_last_error": (ctypes.c_char_p, []),
             "lv_abi_version": (ctypes.c_int, []),
+            "lv_lut_table": (ctypes.c_int, [i32, P(i32)]),
             "lv_encrypt": (ctypes.c_int, [vp, P(i32), sz, P(u32)]),
             "lv_trivial": (ctypes.c_int, [vp, P(i32), sz, P(u32)]),
             "lv_decrypt": (ctypes.c_int, [vp, P(u32), sz, P(i32)]),
@@ -478,14 +479,18 @@ from .leuven import (  # noqa: E402  (reference-shaped pipeline API)
     compute, compute_batch, distance_batch, distance_encrypted, distance_preprocessed,
     distance_preprocessed_batch,
     encrypt_string, load_eq_table, plan_trace, report_json, run_batch, save_eq_table, wf_distance,
+    banded_distance, eq_cost, lut_dump, lut_table,
 )
+
+__version__ = "0.1.0"
 
 __all__ = [
     "Context", "Params", "default_params", "negacyclic_eval", "identity_lut", "eq_lut", "AlphabetSpec",
     "BandSpec", "DistanceRun", "EqTable", "EncryptedString", "band_cell_count", "build_eq_table",
     "compute", "compute_batch", "distance_batch", "distance_encrypted", "distance_preprocessed",
     "distance_preprocessed_batch", "encrypt_string", "plan_trace", "wf_distance", "run_batch",
-    "report_json", "save_eq_table", "load_eq_table", "Error", "OutOfRangeValue", "NoiseBudgetExceeded",
+    "report_json", "save_eq_table", "load_eq_table", "banded_distance", "eq_cost", "lut_dump",
+    "lut_table", "Error", "OutOfRangeValue", "NoiseBudgetExceeded",
     "ValueOutsideLutHalf", "PackingViolation", "CharNotInAlphabet", "CharNotInSubset",
     "PositionOutOfRange", "BandTooNarrow", "FormatError", "InvalidParams", "CudaError", "InvalidHandle",
 ]

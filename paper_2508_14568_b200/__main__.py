@@ -1,12 +1,12 @@
-"""`python -m paper_2508_14568_b200 compute|batch ...` — the reference CLI's
-two ciphertext subcommands (cli.cpp:240-330) on the GPU path.
+"""`python -m paper_2508_14568_b200 compute|batch|table|eqcost ...` — the
+reference CLI's subcommands (cli.cpp:240-330): compute and batch on the GPU
+path, table (the product's own lookup tables) and eqcost (plaintext).
 
 Same flags, LEUVEN_BUDGET default (cli.cpp:131-147), exit codes
 (classify_error_exit, cli.cpp:121-129: 3 band too narrow, 2 input/params,
 1 other) and report formats (print_human_report cli.cpp:110-119,
 report_json cli.cpp:93-107). `--threads` is accepted for compatibility:
-the batch is already traversed as one wavefront over all pairs. The
-plaintext `table` / `eqcost` dumps are outside the GPU path.
+the batch is already traversed as one wavefront over all pairs.
 """
 import argparse
 import os
@@ -69,15 +69,31 @@ def main(argv=None, out=sys.stdout, err=sys.stderr) -> int:
     b.add_argument("--input", required=True)
     b.add_argument("--threads", type=int, default=1)
     _flags(b)
+    tb = sub.add_parser("table", help="dump a lookup table")
+    tb.add_argument("which", help="minlut-original | minlut-negated | eqlut | eqlut9")
+    ec = sub.add_parser("eqcost", help="equality bootstrap-cost table as CSV")
+    ec.add_argument("--max-bits", type=int, default=16, choices=range(1, 65), metavar="[1-64]")
     try:
         args = ap.parse_args(argv)
     except SystemExit as e:
         return 0 if e.code == 0 else 2
+    if args.cmd == "table":  # cli.cpp:212-228
+        if args.which not in ("minlut-original", "minlut-negated", "eqlut", "eqlut9"):
+            err.write(f"unknown table '{args.which}'\n")
+            return 2
+        out.write(leuven.lut_dump(args.which))
+        return 0
+    if args.cmd == "eqcost":  # cli.cpp:230-238
+        out.write("bits,standard,ours,combined\n")
+        for bits in range(1, args.max_bits + 1):
+            out.write(f"{bits},{leuven.eq_cost('standard_2bit', bits)},"
+                      f"{leuven.eq_cost('ours_4bit', bits)},{leuven.eq_cost('combined', bits)}\n")
+        return 0
     try:
         budget = args.budget if args.budget is not None else _env_budget()
         if args.cmd == "compute":
             rep = leuven.compute(args.a, args.b, args.mode, args.ell, args.encoding, budget,
-                                 args.key_encoding, args.preprocess)
+                                 args.key_encoding, args.preprocess, include_timing=True)
             out.write(leuven.report_json(rep, include_timing=True) + "\n" if args.json
                       else _human(rep))
             return 0

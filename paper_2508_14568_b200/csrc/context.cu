@@ -506,6 +506,20 @@ void lv_default_params(lv_params* p) {
 const char* lv_last_error(void) { return g_last_error.c_str(); }
 int lv_abi_version(void) { return LV_ABI_VERSION; }
 
+int lv_lut_table(int32_t which, int32_t* out16) {
+  return guard([&] {
+    std::array<int32_t, 16> e{};
+    switch (which) {
+      case LV_TABLE_MINLUT_ORIGINAL: e = min_lut_entries(false); break;
+      case LV_TABLE_MINLUT_NEGATED: e = min_lut_entries(true); break;
+      case LV_TABLE_EQLUT: e = eq_lut_entries(1); break;
+      case LV_TABLE_EQLUT9: e = eq_lut_entries(9); break;
+      default: throw Error(LV_ERR_INVALID_PARAMS, "unknown table");
+    }
+    std::copy(e.begin(), e.end(), out16);
+  });
+}
+
 int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
   return guard([&] {
     lv_params p;

@@ -14,8 +14,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import (Band, BandTooNarrow, CharNotInAlphabet, Context, InvalidParams, Run, _check, _ptr,
-               _u32, lib)
+from . import (Band, BandTooNarrow, CharNotInAlphabet, Context, InvalidParams, OutOfRangeValue, Run,
+               _check, _ptr, _u32, lib)
 
 # ------------------------------------------------------------ alphabets
 
@@ -120,6 +120,65 @@ def wf_distance(a: str, b: str) -> int:
             cur[j] = prev[j - 1] if a[i - 1] == b[j - 1] else 1 + min(prev[j], cur[j - 1], prev[j - 1])
         prev = cur
     return prev[-1]
+
+
+def banded_distance(a: str, b: str, half_width: int) -> int:
+    """Plaintext banded edit distance (oracle.cpp:55-84): cells outside
+    |i - j| <= half_width stay unreachable, so the result is an upper bound."""
+    m, n = len(a), len(b)
+    if half_width < abs(m - n):
+        raise BandTooNarrow(f"half width {half_width} below length difference {abs(m - n)}")
+    inf = 1 << 30
+    prev = list(range(n + 1))
+    for i in range(1, m + 1):
+        cur = [inf] * (n + 1)
+        cur[0] = i
+        for j in range(max(1, i - half_width), min(n, i + half_width) + 1):
+            diag = prev[j - 1] + (0 if a[i - 1] == b[j - 1] else 1)
+            cur[j] = min(diag, prev[j] + 1, cur[j - 1] + 1)
+        prev = cur
+    return prev[n]
+
+
+def eq_cost(technique: str, bits: int) -> int:
+    """Bootstraps of one character equality (equality.cpp:104-136):
+    standard_2bit | ours_4bit | combined."""
+    if bits < 1:
+        raise OutOfRangeValue("bit width must be positive")
+
+    def merge(k: int) -> int:
+        cost = 0
+        while k > 1:
+            k = (k + 14) // 15
+            cost += k
+        return cost
+
+    if technique == "standard_2bit":
+        k = (bits + 1) // 2
+        return k + merge(k)
+    if technique == "ours_4bit":
+        return 1 if bits <= 4 else 1 + (bits - 4 + 2) // 3
+    if technique == "combined":
+        k = (bits + 3) // 4
+        return k + merge(k)
+    raise InvalidParams(f"unknown equality technique '{technique}'")
+
+
+_TABLES = {"minlut-original": 0, "minlut-negated": 1, "eqlut": 2, "eqlut9": 3}
+
+
+def lut_table(which: str):
+    """The product's own Lut16 entries (lv_lut_table)."""
+    if which not in _TABLES:
+        raise InvalidParams(f"unknown table '{which}'")
+    out = np.zeros(16, np.int32)
+    _check(lib().lv_lut_table(_TABLES[which], _ptr(out, ctypes.c_int32)))
+    return [int(v) for v in out]
+
+
+def lut_dump(which: str) -> str:
+    """Table dump as `cli table` prints it (lut.cpp:24-30): "i<TAB>entry" lines."""
+    return "".join(f"{i}\t{v}\n" for i, v in enumerate(lut_table(which)))
 
 
 # ------------------------------------------------------------ pipeline
@@ -330,7 +389,7 @@ def _context(seed: int, budget: float) -> Context:
 
 def compute(a: str, b: str, mode: str = "exact", ell=None, encoding: str = "ascii7",
             budget: float = 4000.0, key_encoding: str = "negated", preprocess: bool = False,
-            ctx: Context | None = None, seed: int = 0) -> dict:
+            ctx: Context | None = None, seed: int = 0, include_timing: bool = False) -> dict:
     """cli::compute_report (cli.cpp:53-91) / bindings compute(): encrypt ->
     traverse on the GPU -> decrypt; counters as in RunReport (cli.hpp:25-37)."""
     import time
@@ -372,8 +431,8 @@ def compute(a: str, b: str, mode: str = "exact", ell=None, encoding: str = "asci
         "refresh_count": run.refreshes, "preprocessing_pbs": pre_pbs,
         "max_key_variance": run.max_key_variance,
         "linear_ops": after["linear_op_count"] - before["linear_op_count"],
-        "wall_time_ms": (t1 - t0) * 1e3, "waves": run.waves,
-    }
+        "waves": run.waves,
+    } | ({"wall_time_ms": (t1 - t0) * 1e3} if include_timing else {})
 
 
 def compute_batch(pairs, encoding: str = "ascii7", budget: float = 4000.0,

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import json
+import random
 import os
 import sys
 
@@ -59,6 +60,7 @@ def load():
                               ctypes.POINTER(ctypes.c_int32)]
     L.ref_banded_distance.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_uint64,
                                       ctypes.POINTER(ctypes.c_int32)]
+    L.ref_eq_cost.argtypes = [ctypes.c_char_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]
     return L
 
 
@@ -171,6 +173,22 @@ def main():
         trace(L, "kitten", "sitting", mode="approx", ell=2),
         trace(L, "monday", "friday", mode="skip"),
     ]
+    # plaintext helpers of the pybind surface (module.cpp:47-108)
+    v = ctypes.c_int32()
+    out["eq_cost"] = {t: [(L.ref_eq_cost(t.encode(), b, ctypes.byref(v)), v.value)[1]
+                          for b in range(1, 65)]
+                      for t in ("standard_2bit", "ours_4bit", "combined")}
+    rng = random.Random(55)
+    banded = []
+    for _ in range(40):
+        a = "".join(rng.choice("abcdxyz") for _ in range(rng.randint(0, 12)))
+        b = "".join(rng.choice("abcdxyz") for _ in range(rng.randint(0, 12)))
+        hw = rng.randint(0, 12)
+        rc = L.ref_banded_distance(a.encode(), b.encode(), hw, ctypes.byref(v))
+        banded.append({"a": a, "b": b, "half_width": hw,
+                       "distance": v.value if rc == 0 else None,
+                       "error": None if rc == 0 else rc})
+    out["banded"] = banded
     path = os.path.join(HERE, "reference_runs.json")
     with open(path, "w") as f:
         json.dump(out, f, separators=(",", ":"))
