@@ -50,6 +50,9 @@ __device__ __forceinline__ uint32_t swz(uint32_t x) {
 #endif
 constexpr bool kSplitXchg = LVB_SPLIT_XCHG;
 constexpr int kXchgBufs = kSplitXchg ? 1 : 2;
+#ifndef LVB_TW_EARLY
+#define LVB_TW_EARLY 1  // twiddles requested before the exchange that precedes their group
+#endif
 
 // Moves X from layout wr(r) to layout rd(r) (element indices x); the caller
 // guarantees the buffer is free on entry.
@@ -191,9 +194,15 @@ __device__ __forceinline__ double2 shfl_xor_d2(double2 v, int m) {
 // ---------------------------------------------------------------- forward
 // X[p][r] on entry: twisted inputs at x = t + 128 r. On exit: spectrum
 // bins 8t + r. buf: the exchange buffer(s).
-template <int P>
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+// hook() runs once group C's data has arrived (the caller issues loads it
+// needs right after the transform there, e.g. the first BSK row).
+template <int P, typename Hook = NoHook>
 __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
-                                            const double2* __restrict__ tw, uint32_t t) {
+                                            const double2* __restrict__ tw, uint32_t t,
+                                            Hook hook = Hook()) {
   // group A: radix-4 (0,1) with k = t + 128 r, radix-2 stage 2
   {
     double2 w[2][3];
@@ -215,6 +224,15 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
   // A -> B: radix-4 (3,4) with j = u + 16 r, radix-2 stage 5
   {
     const uint32_t b = t >> 4, u = t & 15;
+#if LVB_TW_EARLY
+    double2 w[2][3];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 3, m + 1, u + 16 * r);
+    xchg<P>(X, buf, [&](int r) { return t + 128 * r; },
+            [&](int r) { return 128 * b + u + 16 * r; });
+#else
     xchg<P>(X, buf, [&](int r) { return t + 128 * r; },
             [&](int r) { return 128 * b + u + 16 * r; });
     double2 w[2][3];
@@ -222,6 +240,7 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
     for (int r = 0; r < 2; ++r)
 #pragma unroll
       for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 3, m + 1, u + 16 * r);
+#endif
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -232,10 +251,21 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; r += 2) dif(X[p][r], X[p][r + 1], w5);
+#if LVB_TW_EARLY
+    const uint32_t v0 = t & 1;
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 6, m + 1, v0 + 2 * r);
+#endif
     __syncthreads();
     const uint32_t c = t >> 1, v = t & 1;
     xchg<P>(X, buf, [&](int r) { return 128 * b + u + 16 * r; },
             [&](int r) { return 16 * c + v + 2 * r; });
+    hook();
+#if LVB_TW_EARLY
+    // group C continues in this scope (w already holds its twiddles)
+#else
   }
   // C: radix-4 (6,7) with j = v + 2 r, radix-2 stage 8, stage 9 by shuffle
   {
@@ -245,6 +275,7 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
     for (int r = 0; r < 2; ++r)
 #pragma unroll
       for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 6, m + 1, v + 2 * r);
+#endif
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -296,19 +327,31 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
     }
   }
   const uint32_t b = t >> 3, u = t & 7, odd = b & 1;
+#if LVB_TW_EARLY
+  const double2 w6 = tws(tw, 6, u);
+  double2 w[2][3];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 4, m + 1, u + 8 * r);
+#endif
   xchg<P>(X, buf, [&](int r) { return 8 * t + r; }, [&](int r) { return 64 * b + u + 8 * r; });
   {
     // stage 6, radix-4 (5,4) with j = u + 8 r
+#if !LVB_TW_EARLY
     const double2 w6 = tws(tw, 6, u);
+#endif
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w6);
+#if !LVB_TW_EARLY
     double2 w[2][3];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
       for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 4, m + 1, u + 8 * r);
+#endif
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -339,6 +382,13 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
       for (int q = 0; q < 8; ++q) X[p][q] = Z[q];
     }
   }
+#if LVB_TW_EARLY
+  const double2 w2 = tws(tw, 2, t);
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 0, m + 1, t + 128 * r);
+#endif
   __syncthreads();
   xchg<P>(
       X, buf,
@@ -346,16 +396,20 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
       [&](int r) { return t + 128 * r; });
   {
     // stage 2, radix-4 (1,0) with j = t + 128 r
+#if !LVB_TW_EARLY
     const double2 w2 = tws(tw, 2, t);
+#endif
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w2);
+#if !LVB_TW_EARLY
     double2 w[2][3];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
       for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 0, m + 1, t + 128 * r);
+#endif
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -372,7 +426,7 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
 // yields d = -2^63 instead of +2^63 - 2^64 — the same residue — so no tie
 // fix-up is needed, and d = y - r 2^64 is one exact FMA.
 __device__ __forceinline__ uint64_t f64_to_torus(double y) {
-  const double r = floor(__dadd_rn(__dmul_rn(y, 0x1p-64), 0.5));
+  const double r = floor(__fma_rn(y, 0x1p-64, 0.5));  // the product is exact
   const double d = __fma_rn(-r, 18446744073709551616.0, y);
   return (uint64_t)__double2ll_rn(d);
 }

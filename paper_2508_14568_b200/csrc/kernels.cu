@@ -84,6 +84,9 @@ __device__ __forceinline__ double2 mac2(double2 d0, double2 b0, double2 d1, doub
 //
 // Shared memory: acc[2][N] u64 (32 KB) + FFT exchange buffer kXchgBufs x kM
 // double2 (16 KB) + ms[n+1] u16. 168 registers, 3 CTAs/SM.
+#ifndef LVB_BSK_EARLY
+#define LVB_BSK_EARLY 2  // BSK bin groups requested inside the forward transform
+#endif
 template <bool kExact>
 __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -115,6 +118,9 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
   // updates exactly the coefficients it decomposed; shared memory serves
   // the rotated reads of the other threads.
   const double2 tw_fine = __ldg(a.twist + t);  // twist of x = t + 128 r is fine[t] * coarse[r]
+// (formed, not loaded: a 1024-entry twist table read through L1 measured
+// 92 vs 72 ms per 4096 — the L1 data pipe is the scarcer resource)
+#define TWIST_R(r) ((r) == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]))
   __syncthreads();
   uint64_t own[2][16];  // [poly][2 r + half]
 #pragma unroll
@@ -146,12 +152,29 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
           const uint64_t rv = s < kN ? pv : (uint64_t)0 - pv;
           d[hpart] = (int32_t)decomp1(rv - own[p][2 * r + hpart], kPbsBaseLog);
         }
-        const double2 tz = r == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]);
+        const double2 tz = TWIST_R(r);
         X[p][r] = cmul(make_double2((double)d[0], (double)d[1]), tz);
       }
     }
 
+#if LVB_BSK_EARLY
+    // the first bins' BSK values are requested before the transform's last
+    // group so their L2 latency overlaps it
+    double2 bpre[LVB_BSK_EARLY][kExact ? 6 : 4];
+    const double2* bsk_row =
+        a.bskf + (size_t)i * (8 * (kExact ? 6 : 4) * 128) + t;
+    fft_forward<2>(X, buf, tw, t, [&] {
+#pragma unroll
+      for (int q = 0; q < LVB_BSK_EARLY; ++q)
+#pragma unroll
+        for (int e = 0; e < (kExact ? 6 : 4); ++e)
+          bpre[q][e] = ld_stream(bsk_row + (q * (kExact ? 6 : 4) + e) * 128);
+    });
+#define BSK_AT(q, e, ptr) ((q) < LVB_BSK_EARLY ? bpre[(q) < LVB_BSK_EARLY ? (q) : 0][e] : ld_stream(ptr))
+#else
     fft_forward<2>(X, buf, tw, t);
+#define BSK_AT(q, e, ptr) ld_stream(ptr)
+#endif
 
     // pointwise MAC against BSK_i (bins 8t + q), then the inverse transforms;
     // untwist (conj(twist); the 1/M is pre-applied to the BSK), back to the
@@ -166,8 +189,9 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
       for (int q = 0; q < 8; ++q) {
         const double2* bq = bsk + q * (6 * 128);
         const double2 d0 = X[0][q], d1 = X[1][q];
-        const double2 h0 = ld_stream(bq), l0 = ld_stream(bq + 128), b0 = ld_stream(bq + 256);
-        const double2 h1 = ld_stream(bq + 384), l1 = ld_stream(bq + 512), b1 = ld_stream(bq + 640);
+        const double2 h0 = BSK_AT(q, 0, bq), l0 = BSK_AT(q, 1, bq + 128), b0 = BSK_AT(q, 2, bq + 256);
+        const double2 h1 = BSK_AT(q, 3, bq + 384), l1 = BSK_AT(q, 4, bq + 512),
+                      b1 = BSK_AT(q, 5, bq + 640);
         Z[0][q] = mac2(d0, h0, d1, h1);
         Z[1][q] = mac2(d0, l0, d1, l1);
         Z[2][q] = mac2(d1, b1, d0, b0);  // body output: row 1 first
@@ -176,7 +200,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
       fft_inverse_a<3>(Z, buf, tw, t);
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        const double2 tv = r == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]);
+        const double2 tv = TWIST_R(r);
         const double2 ut = make_double2(tv.x, -tv.y);
         const uint32_t x = t + 128 * r;
         const double2 zh = cmul(Z[0][r], ut), zl = cmul(Z[1][r], ut), zb = cmul(Z[2][r], ut);
@@ -196,8 +220,8 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
       for (int q = 0; q < 8; ++q) {
         const double2* bq = bsk + q * (4 * 128);
         const double2 d0 = X[0][q], d1 = X[1][q];
-        const double2 b00 = ld_stream(bq), b01 = ld_stream(bq + 128);
-        const double2 b10 = ld_stream(bq + 256), b11 = ld_stream(bq + 384);
+        const double2 b00 = BSK_AT(q, 0, bq), b01 = BSK_AT(q, 1, bq + 128);
+        const double2 b10 = BSK_AT(q, 2, bq + 256), b11 = BSK_AT(q, 3, bq + 384);
         X[0][q] = mac2(d0, b00, d1, b10);
         X[1][q] = mac2(d1, b11, d0, b01);  // output o: row o first
       }
@@ -205,7 +229,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
       fft_inverse_a<2>(X, buf, tw, t);
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        const double2 tv = r == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]);
+        const double2 tv = TWIST_R(r);
         const double2 ut = make_double2(tv.x, -tv.y);
         const uint32_t x = t + 128 * r;
 #pragma unroll
@@ -221,6 +245,8 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
       }
     }
   }
+#undef BSK_AT
+#undef TWIST_R
   __syncthreads();
 
   if (a.glwe_out)  // debug / noise measurement: the whole accumulator
