@@ -74,6 +74,22 @@ def test_pbs_bit_exact_all_luts(ctx, orc, golden):
         assert orc.decrypt(got[i]) == L.negacyclic_eval(luts[which[i]], int(x))
 
 
+def test_pbs_host_equals_device_path(ctx, golden):
+    # 2000 items (several blind-rotation waves, mixed LUTs): the host-buffer
+    # entry point must equal the handle path bit for bit, in order
+    luts = [golden["luts"][n] for n in ("identity", "minlut-negated", "eqlut9")]
+    ids = np.array([ctx.lut(l) for l in luts], np.uint32)
+    vals = [(7 * i) % 16 for i in range(2000)]
+    cts = ctx.encrypt(vals)
+    rows = ctx.export(cts)
+    which = ids[np.arange(2000) % 3]
+    got = ctx.pbs_host(rows, which)
+    dev = ctx.pbs(cts, lut_ids=which)
+    assert np.array_equal(got, ctx.export(dev))
+    ctx.release(cts)
+    ctx.release(dev)
+
+
 def test_pbs_handles_budget_and_counters(golden):
     c = L.Context(seed=5, budget=25.0)  # NoiseParams::tight(), backend.hpp:29
     lut = [(x - 4 + 16) % 16 for x in range(16)]  # test_backend.cpp:16-24
