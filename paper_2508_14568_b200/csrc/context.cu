@@ -1,6 +1,7 @@
 // Host runtime: context lifecycle and key generation, the device ciphertext
 // pool, the Backend operations (proj/include/leuven/backend.hpp:54-76) and
 // the batched PBS driver, exposed through the C ABI in include/leuven_b200.h.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -198,7 +199,7 @@ void launch_blind_rotate(lv_ctx* c, const BrArgs& ba, uint32_t count) {
 }
 
 void launch_pbs_dev(lv_ctx* c, const LinDesc* d_desc, const uint32_t* d_lut, const BrOut* d_out,
-                    uint32_t count, cudaEvent_t ks_done) {
+                    uint32_t count, cudaEvent_t ks_done, uint32_t* done, uint32_t done_chunk) {
   if (!count) return;
   const uint32_t stride = ms_stride(c);
   uint16_t* d_ms = c->ms.get((size_t)count * stride);
@@ -206,6 +207,8 @@ void launch_pbs_dev(lv_ctx* c, const LinDesc* d_desc, const uint32_t* d_lut, con
   if (ks_done) LV_CUDA(cudaEventRecord(ks_done, c->stream));
   BrArgs ba{d_ms, stride, d_lut, c->d_tp, c->d_bskf, c->d_tw, c->d_twist, c->p.n,
             c->d_pool, kBigStride, d_out};
+  ba.done = done;
+  ba.done_chunk = done_chunk;
   launch_blind_rotate(c, ba, count);
 }
 
@@ -292,16 +295,20 @@ static void upload_rows(lv_ctx* c, const uint64_t* host, const std::vector<lv_ct
   }
 }
 
-static void download_rows(lv_ctx* c, const std::vector<lv_ct>& slots, uint64_t* host) {
+static void download_rows_on(lv_ctx* c, cudaStream_t st, const std::vector<lv_ct>& slots,
+                             uint64_t* host) {
   size_t i = 0;
   while (i < slots.size()) {
     size_t j = i + 1;
     while (j < slots.size() && slots[j] == slots[j - 1] + 1) ++j;
     LV_CUDA(cudaMemcpy2DAsync(host + i * (kBig + 1), (kBig + 1) * 8,
                               c->d_pool + (size_t)slots[i] * kBigStride, kBigStride * 8,
-                              (kBig + 1) * 8, j - i, cudaMemcpyDeviceToHost, c->stream));
+                              (kBig + 1) * 8, j - i, cudaMemcpyDeviceToHost, st));
     i = j;
   }
+}
+static void download_rows(lv_ctx* c, const std::vector<lv_ct>& slots, uint64_t* host) {
+  download_rows_on(c, c->stream, slots, host);
 }
 
 static std::vector<uint64_t> phases(lv_ctx* c, const lv_ct* cts, size_t count) {
@@ -544,6 +551,7 @@ int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
       c->seed = seed;
       LV_CUDA(cudaGetDevice(&c->device));
       LV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      LV_CUDA(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
       LV_CUDA(cudaFuncSetAttribute(blind_rotate_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)blind_rotate_smem_bytes(p.n, false)));
@@ -563,6 +571,14 @@ int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
         c->br_pair_max = (uint32_t)sms;
         if (const char* e = std::getenv("LVB_BR_PAIR_MAX"))
           c->br_pair_max = (uint32_t)std::strtoul(e, nullptr, 10);
+        int per_sm = 1;
+        if (p.exact_mask_product)
+          LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+              &per_sm, blind_rotate_exact_kernel, 128, blind_rotate_smem_bytes(p.n, true)));
+        else
+          LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+              &per_sm, blind_rotate_kernel, 128, blind_rotate_smem_bytes(p.n, false)));
+        c->br_slots = (uint32_t)(sms * std::max(per_sm, 1));
       }
       build_tables(c);
       keygen(c);
@@ -600,6 +616,7 @@ void lv_ctx_destroy(lv_ctx* c) {
   c->u64a.release();
   c->u64b.release();
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->copy_out) cudaStreamDestroy(c->copy_out);
   delete c;
 }
 
@@ -804,37 +821,79 @@ int lv_import(lv_ctx* c, const uint64_t* host, size_t count, lv_ct* out) {
   });
 }
 
+// cuStreamWaitValue32 through the runtime's driver entry point (no libcuda
+// link dependency); null when the driver does not offer stream memory ops.
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WaitValueFn wait_value_fn() {
+  static WaitValueFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (WaitValueFn) nullptr;
+    return reinterpret_cast<WaitValueFn>(f);
+  }();
+  return fn;
+}
+
+// Host batch: upload, one key switch + one blind rotation launch (one long
+// launch keeps the kernel in its steady state: chunked launches measured
+// slower), and downloads that start while the launch is still running —
+// the blind rotation counts finished CTAs per chunk of br_slots items
+// (BrArgs::done) and the copy stream waits on each chunk's counter
+// (cuStreamWaitValue32) before copying its rows back.
 int lv_pbs_batch_host(lv_ctx* c, const uint64_t* in, const uint32_t* luts, size_t count,
                       uint64_t* out) {
   return guard([&] {
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     for (size_t i = 0; i < count; ++i)
       if (luts[i] >= c->luts.size()) throw Error(LV_ERR_INVALID_PARAMS, "unknown lut id");
+    if (!count) return;
     std::vector<lv_ct> s = pool_alloc(c, count);
     upload_rows(c, in, s);
-    std::vector<PbsItem> items(count);
-    for (size_t i = 0; i < count; ++i) {
-      items[i].in = single(s[i]);
-      items[i].lut = luts[i];
-      items[i].out = BrOut{0, s[i], kNoSlot, kNoSlot, kNoSlot, 0};  // in place: KS reads first
-    }
     std::vector<LinDesc> d(count);
-    std::vector<uint32_t> l(count);
     std::vector<BrOut> o(count);
     for (size_t i = 0; i < count; ++i) {
-      d[i] = items[i].in;
-      l[i] = items[i].lut;
-      o[i] = items[i].out;
+      d[i] = single(s[i]);
+      o[i] = BrOut{0, s[i], kNoSlot, kNoSlot, kNoSlot, 0};  // in place: KS reads first
     }
     LinDesc* dd = c->desc.get(count);
     uint32_t* dl = c->lut_item.get(count);
     BrOut* dout = c->br_out.get(count);
     LV_CUDA(cudaMemcpyAsync(dd, d.data(), count * sizeof(LinDesc), cudaMemcpyHostToDevice, c->stream));
-    LV_CUDA(cudaMemcpyAsync(dl, l.data(), count * 4, cudaMemcpyHostToDevice, c->stream));
+    LV_CUDA(cudaMemcpyAsync(dl, luts, count * 4, cudaMemcpyHostToDevice, c->stream));
     LV_CUDA(cudaMemcpyAsync(dout, o.data(), count * sizeof(BrOut), cudaMemcpyHostToDevice, c->stream));
-    launch_pbs_dev(c, dd, dl, dout, (uint32_t)count);
-    download_rows(c, s, out);
-    LV_CUDA(cudaStreamSynchronize(c->stream));
+    const WaitValueFn wait = wait_value_fn();
+    const size_t chunk = std::max<size_t>(c->br_slots, 1);
+    const bool overlap = wait && count > c->br_pair_max && count >= 2 * chunk &&
+                         std::getenv("LVB_HOST_NO_OVERLAP") == nullptr;
+    if (!overlap) {
+      launch_pbs_dev(c, dd, dl, dout, (uint32_t)count);
+      download_rows(c, s, out);
+      LV_CUDA(cudaStreamSynchronize(c->stream));
+    } else {
+      const size_t nchunks = (count + chunk - 1) / chunk;
+      uint32_t* done = c->u32b.get(nchunks);
+      LV_CUDA(cudaMemsetAsync(done, 0, nchunks * 4, c->stream));
+      cudaEvent_t zeroed;
+      LV_CUDA(cudaEventCreateWithFlags(&zeroed, cudaEventDisableTiming));
+      LV_CUDA(cudaEventRecord(zeroed, c->stream));
+      // the copy stream must not see the previous call's counters
+      LV_CUDA(cudaStreamWaitEvent(c->copy_out, zeroed, 0));
+      launch_pbs_dev(c, dd, dl, dout, (uint32_t)count, nullptr, done, (uint32_t)chunk);
+      for (size_t k = 0; k < nchunks; ++k) {
+        const size_t off = k * chunk, m = std::min(chunk, count - off);
+        if (wait(reinterpret_cast<CUstream>(c->copy_out),
+                 reinterpret_cast<CUdeviceptr>(done + k), (cuuint32_t)m,
+                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+          throw Error(LV_ERR_CUDA, "cuStreamWaitValue32 failed");
+        std::vector<lv_ct> sk(s.begin() + off, s.begin() + off + m);
+        download_rows_on(c, c->copy_out, sk, out + off * (kBig + 1));
+      }
+      LV_CUDA(cudaStreamSynchronize(c->copy_out));
+      LV_CUDA(cudaStreamSynchronize(c->stream));
+      cudaEventDestroy(zeroed);
+    }
     pool_free(c, s.data(), count);
     c->pbs_count += count;
   });

@@ -66,6 +66,7 @@ struct lv_ctx {
   lv_params p{};
   uint64_t seed = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_out = nullptr;  // lv_pbs_batch_host: chunk downloads behind the compute
   int device = 0;
   std::recursive_mutex mu;
 
@@ -113,6 +114,7 @@ struct lv_ctx {
   std::map<std::string, lvb::PairPlan> plan_cache;
   uint32_t min_lut[2] = {0, 0};
   uint32_t br_pair_max = 0;  // waves up to this size run blind_rotate_pair_kernel
+  uint32_t br_slots = 0;     // blind-rotation CTAs resident on the whole GPU at once
   uint32_t identity_lut = 0;
 };
 
@@ -129,7 +131,8 @@ uint32_t lut_id(lv_ctx* c, const std::array<int32_t, 16>& e);
 // uploaded here; pool slots must already exist.
 void run_pbs_items(lv_ctx* c, const std::vector<PbsItem>& items);
 void launch_pbs_dev(lv_ctx* c, const LinDesc* d_desc, const uint32_t* d_lut, const BrOut* d_out,
-                    uint32_t count, cudaEvent_t ks_done = nullptr);
+                    uint32_t count, cudaEvent_t ks_done = nullptr, uint32_t* done = nullptr,
+                    uint32_t done_chunk = 1);
 void run_linear(lv_ctx* c, const std::vector<LinOut>& ops);
 void launch_linear_dev(lv_ctx* c, const LinOut* d_ops, uint32_t count);
 

@@ -56,6 +56,18 @@ __device__ __forceinline__ void br_output(const BrOut& o, uint64_t* pool, uint32
   if (o.snap_dh != kNoSlot) pool[(size_t)o.snap_dh * S + j] = h_out;
 }
 
+// Completion counter of the item's chunk (BrArgs::done): after every
+// thread's output stores, one thread fences them to device scope and counts
+// the CTA, so a copy stream waiting on the counter reads finished rows.
+__device__ __forceinline__ void signal_done(const BrArgs& a, uint32_t item) {
+  if (!a.done) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(a.done + item / a.done_chunk, 1u);
+  }
+}
+
 // o = d0 * b0 + d1 * b1 for one spectrum bin, in the MAC's fixed FMA order
 // (oracle mac_bins): the first pair first, real part first. Output o takes
 // row o first (rows rotated), so each polynomial's own term leads.
@@ -257,6 +269,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
   for (uint32_t j = t; j <= kN; j += 128)
     br_output(o, a.pool, a.pool_stride, j,
               j == 0 ? acc[0] : (j == kN ? acc[kN] : (uint64_t)0 - acc[kN - j]));
+  signal_done(a, item);
 }
 #ifndef LVB_BR_CTAS
 #define LVB_BR_CTAS 3  // resident CTAs per SM the register allocation targets
@@ -437,6 +450,7 @@ blind_rotate_pair_kernel(BrArgs a) {
   const uint32_t j0 = p == 0 ? t : kN + t, j1 = p == 0 ? kN : kN + 1;
   for (uint32_t j = j0; j < j1; j += 128)
     br_output(o, a.pool, a.pool_stride, j, j == 0 || j == kN ? acc[0] : (uint64_t)0 - acc[kN - j]);
+  signal_done(a, item);
 }
 
 // acc (16 KB) + exchange buffer (16 KB) + 2 published spectra (32 KB) + ms.

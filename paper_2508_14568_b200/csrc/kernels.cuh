@@ -58,6 +58,11 @@ struct BrArgs {
   uint32_t pool_stride;
   const BrOut* outs;           // [count]
   uint64_t* glwe_out = nullptr;  // debug: full accumulator [count][2][N] (noise tests)
+  // optional completion counters, one per done_chunk items: each CTA adds 1
+  // after its outputs are globally visible (lv_pbs_batch_host downloads a
+  // chunk as soon as its counter is full)
+  uint32_t* done = nullptr;
+  uint32_t done_chunk = 1;
 };
 
 struct KsArgs {
