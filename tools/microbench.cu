@@ -63,6 +63,44 @@ __global__ void k_dfma(double* out, int iters) {
   if (s == -1) out[0] = s;
 }
 
+// LDS.128 and SHFL in the same SM: even warps run the k_lds loop, odd
+// warps the k_shfl loop (does SHFL share the shared-memory data pipe?)
+__global__ void k_mix(double* out, int iters, int mode) {
+  __shared__ double2 buf[2048];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) buf[i] = make_double2(i, i);
+  __syncthreads();
+  const int w = threadIdx.x / 32;
+  const bool lds = mode == 0 ? true : mode == 1 ? false : (w & 1) == 0;
+  if ((mode == 3 && (w & 1)) ) return;  // mode 3: only the even (LDS) half runs
+  if ((mode == 4 && !(w & 1))) return;  // mode 4: only the odd (SHFL) half runs
+  double s = 0;
+  if (mode == 3 || (mode == 2 && lds) || mode == 0) {
+    double2 acc = make_double2(0, 0);
+    unsigned idx = threadIdx.x;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        double2 v = buf[(idx + k * 128) & 2047];
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+      idx += 32;
+    }
+    s = acc.x + acc.y;
+  } else {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = threadIdx.x + k;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = __shfl_xor_sync(0xffffffffu, a[k], 1 + (k & 7));
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+  }
+  if (s == -1) out[0] = s;
+}
+
 // TMEM: each warp stores/loads 32 lanes x 32 columns (x32) repeatedly.
 __global__ void k_tmem(unsigned* out, int iters, int do_load) {
   __shared__ unsigned taddr_s;
@@ -155,6 +193,14 @@ int main() {
     printf("tcgen05.%s 32x32b.x32: %.3f warp-instr/clk/SM = %.1f B/clk/SM (err=%s)\n", ld ? "ld" : "st",
            ops / (ms * 1e-3) / sms / (clk * 1e3), ops * 4096 / (ms * 1e-3) / sms / (clk * 1e3),
            cudaGetErrorString(cudaGetLastError()));
+  }
+  {
+    const char* nm[5] = {"all LDS", "all SHFL", "half LDS + half SHFL", "half LDS only",
+                         "half SHFL only"};
+    for (int m = 0; m < 5; ++m) {
+      ms = timeit([&] { k_mix<<<sms * 4, 256>>>(d, iters, m); });
+      printf("mix %-22s %.3f ms\n", nm[m], ms);
+    }
   }
   printf("clock %d kHz (nominal attr)\n", clk);
   return 0;
