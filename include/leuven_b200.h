@@ -62,7 +62,7 @@ typedef struct {
                                 * H 2^43 + Lo with an exactly rounded H product, so
                                 * the FFT adds no key-amplified noise (phase-noise
                                 * variance within 1.001x of exact integer products;
-                                * 1.47x blind-rotation time). DESIGN.md §2. */
+                                * 1.4x blind-rotation time). DESIGN.md §2. */
 } lv_params;
 
 typedef struct lv_ctx lv_ctx;
@@ -97,6 +97,22 @@ void lv_default_params(lv_params* out);
 /* Generates secret keys, KSK and BSK on the device from `seed` (Philox). */
 int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out);
 void lv_ctx_destroy(lv_ctx* ctx);
+/* Client / server split (new surface). A context made by lv_ctx_create
+ * holds the secret keys; lv_keys_export copies its evaluation keys to host
+ * buffers of lv_keys_size words — the BSK in the standard domain,
+ * [i < n][row < 2][poly < 2][N] u64 (GGSW rows of s_i under the GLWE key),
+ * and the KSK [j < N][level < 5][n + 1] u64 — plus the key-set id (the
+ * generating seed) that LEQT tables carry. lv_ctx_create_eval builds an
+ * evaluation-only context from them (the Fourier BSK is computed on the
+ * device): every homomorphic entry point works, while lv_encrypt,
+ * lv_decrypt, lv_phase and the secret parts of lv_debug_keys fail with
+ * LV_ERR_INVALID_PARAMS, and lv_refresh_batch skips the plaintext-range
+ * check it cannot perform. Ciphertexts move between the two contexts with
+ * lv_export / lv_import; results are bit-identical to the client's own. */
+int lv_keys_size(const lv_params* params, uint64_t* bsk_count, uint64_t* ksk_count);
+int lv_keys_export(lv_ctx* ctx, uint64_t* bsk, uint64_t* ksk, uint64_t* key_id);
+int lv_ctx_create_eval(const lv_params* params, const uint64_t* bsk, const uint64_t* ksk,
+                       uint64_t key_id, lv_ctx** out);
 const char* lv_last_error(void);
 int lv_abi_version(void);
 

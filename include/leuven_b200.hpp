@@ -13,6 +13,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <memory>
 #include <vector>
 
 #include "leuven_b200.h"
@@ -64,7 +65,7 @@ struct StatsSnapshot {  // backend.hpp:36-40
 // each also available in batched form.
 class GpuBackend {
  public:
-  // exact_mask_product: see lv_params (noise of exact products, 1.47x time)
+  // exact_mask_product: see lv_params (noise of exact products, 1.4x time)
   explicit GpuBackend(double budget = 4000.0, uint64_t seed = 0, bool exact_mask_product = false) {
     lv_params p;
     lv_default_params(&p);
@@ -75,6 +76,39 @@ class GpuBackend {
   ~GpuBackend() { lv_ctx_destroy(ctx_); }
   GpuBackend(const GpuBackend&) = delete;
   GpuBackend& operator=(const GpuBackend&) = delete;
+
+  // Client / server split: the evaluation keys of a secret-holding backend
+  // (lv_keys_export) and a server backend built from them, which has no
+  // secret key (encrypt/decrypt throw InvalidParams).
+  struct EvalKeys {
+    std::vector<uint64_t> bsk, ksk;
+    uint64_t key_id = 0;
+  };
+  EvalKeys export_keys() const {
+    lv_params p;
+    check(lv_get_params(ctx_, &p));
+    uint64_t nb = 0, nk = 0;
+    check(lv_keys_size(&p, &nb, &nk));
+    EvalKeys k;
+    k.bsk.resize(nb);
+    k.ksk.resize(nk);
+    check(lv_keys_export(ctx_, k.bsk.data(), k.ksk.data(), &k.key_id));
+    return k;
+  }
+  static std::unique_ptr<GpuBackend> evaluation(const EvalKeys& k, double budget = 4000.0,
+                                                bool exact_mask_product = false) {
+    lv_params p;
+    lv_default_params(&p);
+    p.max_variance_budget = budget;
+    p.exact_mask_product = exact_mask_product ? 1u : 0u;
+    uint64_t nb = 0, nk = 0;
+    check(lv_keys_size(&p, &nb, &nk));
+    if (k.bsk.size() != nb || k.ksk.size() != nk)
+      throw InvalidParams("evaluation keys have the wrong size");
+    lv_ctx* c = nullptr;
+    check(lv_ctx_create_eval(&p, k.bsk.data(), k.ksk.data(), k.key_id, &c));
+    return std::unique_ptr<GpuBackend>(new GpuBackend(c));
+  }
 
   lv_ctx* raw() const { return ctx_; }
 
@@ -144,6 +178,7 @@ class GpuBackend {
   void release(const std::vector<Ct>& cs) { check(lv_release(ctx_, cs.data(), cs.size())); }
 
  private:
+  explicit GpuBackend(lv_ctx* c) : ctx_(c) {}
   template <typename F>
   Ct one(F f, int v) {
     int32_t x = v;

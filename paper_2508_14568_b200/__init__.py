@@ -112,6 +112,7 @@ class Run(ctypes.Structure):
 # Every exported symbol declared in include/leuven_b200.h (checked by tests).
 EXPORTS = [
     "lv_default_params", "lv_ctx_create", "lv_ctx_destroy", "lv_last_error", "lv_abi_version",
+    "lv_keys_size", "lv_keys_export", "lv_ctx_create_eval",
     "lv_lut_table", "lv_encrypt", "lv_trivial", "lv_decrypt", "lv_add", "lv_sub", "lv_scalar_mul",
     "lv_scalar_add", "lv_lut_upload", "lv_pbs_batch", "lv_refresh_batch", "lv_predict_variance",
     "lv_get_stats", "lv_get_params", "lv_release", "lv_ledger_variance", "lv_export",
@@ -145,6 +146,9 @@ def lib():
         sig = {
             "lv_default_params": (None, [P(Params)]),
             "lv_ctx_create": (ctypes.c_int, [P(Params), u64, P(vp)]),
+            "lv_keys_size": (ctypes.c_int, [P(Params), P(u64), P(u64)]),
+            "lv_keys_export": (ctypes.c_int, [vp, P(u64), P(u64), P(u64)]),
+            "lv_ctx_create_eval": (ctypes.c_int, [P(Params), P(u64), P(u64), u64, P(vp)]),
             "lv_ctx_destroy": (None, [vp]),
             "lv_last_error": (ctypes.c_char_p, []),
             "lv_abi_version": (ctypes.c_int, []),
@@ -265,17 +269,53 @@ class Context:
     scalars or arrays and is batched underneath.
     """
 
-    def __init__(self, seed: int = 0, params: Params | None = None, budget: float | None = None):
+    def __init__(self, seed: int = 0, params: Params | None = None, budget: float | None = None,
+                 _eval_keys=None):
         p = params if params is not None else default_params()
         if budget is not None:
             p.max_variance_budget = float(budget)
         self.params = p
         self.seed = seed
         h = ctypes.c_void_p()
-        _check(lib().lv_ctx_create(ctypes.byref(p), seed, ctypes.byref(h)))
+        if _eval_keys is None:
+            _check(lib().lv_ctx_create(ctypes.byref(p), seed, ctypes.byref(h)))
+        else:
+            bsk, ksk, key_id = _eval_keys
+            _check(lib().lv_ctx_create_eval(ctypes.byref(p), _ptr(bsk, ctypes.c_uint64),
+                                            _ptr(ksk, ctypes.c_uint64), int(key_id),
+                                            ctypes.byref(h)))
         self._h = h
         self.n, self.N = p.n, p.N
         self.row = p.k * p.N + 1
+
+    # client / server split -------------------------------------------
+    def export_keys(self):
+        """Evaluation keys of this (secret-holding) context: (bsk, ksk, key_id),
+        the BSK in the standard domain [n][2][2][N] and the KSK [N][5][n+1]
+        as uint64 arrays (lv_keys_export)."""
+        nb, nk = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().lv_keys_size(ctypes.byref(self.params), ctypes.byref(nb), ctypes.byref(nk)))
+        bsk = np.zeros(nb.value, np.uint64)
+        ksk = np.zeros(nk.value, np.uint64)
+        kid = ctypes.c_uint64()
+        _check(lib().lv_keys_export(self._h, _ptr(bsk, ctypes.c_uint64), _ptr(ksk, ctypes.c_uint64),
+                                    ctypes.byref(kid)))
+        return bsk, ksk, kid.value
+
+    @classmethod
+    def evaluation(cls, bsk, ksk, key_id: int, params: Params | None = None,
+                   budget: float | None = None) -> "Context":
+        """A server context from a client's evaluation keys (lv_ctx_create_eval):
+        no secret key, so encrypt/decrypt/phase raise InvalidParams."""
+        p = params if params is not None else default_params()
+        nb, nk = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().lv_keys_size(ctypes.byref(p), ctypes.byref(nb), ctypes.byref(nk)))
+        b = np.ascontiguousarray(bsk, np.uint64).reshape(-1)
+        k = np.ascontiguousarray(ksk, np.uint64).reshape(-1)
+        if b.size != nb.value or k.size != nk.value:
+            raise InvalidParams(f"evaluation keys: expected {nb.value} BSK and {nk.value} KSK words, "
+                                f"got {b.size} and {k.size}")
+        return cls(seed=0, params=p, budget=budget, _eval_keys=(b, k, key_id))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -311,7 +311,14 @@ static void download_rows(lv_ctx* c, const std::vector<lv_ct>& slots, uint64_t* 
   download_rows_on(c, c->stream, slots, host);
 }
 
+static void need_secret(const lv_ctx* c) {
+  if (!c->d_sk_glwe)
+    throw Error(LV_ERR_INVALID_PARAMS,
+                "evaluation-only context (lv_ctx_create_eval) holds no secret key");
+}
+
 static std::vector<uint64_t> phases(lv_ctx* c, const lv_ct* cts, size_t count) {
+  need_secret(c);
   std::vector<uint64_t> ph(count);
   if (!count) return ph;
   uint32_t* ds = c->u32a.get(count);
@@ -392,33 +399,34 @@ static void build_tables(lv_ctx* c) {
   LV_CUDA(cudaMemcpy(c->d_twist, twist.data(), twist.size() * sizeof(double2), cudaMemcpyHostToDevice));
 }
 
-static void keygen(lv_ctx* c) {
+static size_t bsk_words(uint32_t n) { return (size_t)n * kRows * (kK + 1) * kN; }
+static size_t ksk_words(uint32_t n) { return (size_t)kBig * kKsLevel * (n + 1); }
+
+// Everything the key switch derives from the KSK (c->d_ksk): the bias row
+// and the byte limbs of the tensor-core GEMM, with its TMA tensor map.
+static void derive_ksk(lv_ctx* c) {
   const uint32_t n = c->p.n;
-  LV_CUDA(cudaMalloc(&c->d_sk_small, n));
-  LV_CUDA(cudaMalloc(&c->d_sk_glwe, kBig));
-  keygen_secret_kernel<<<(std::max(n, kBig) + 255) / 256, 256, 0, c->stream>>>(c->seed, n, c->d_sk_small,
-                                                                              c->d_sk_glwe);
-  LV_CUDA(cudaGetLastError());
-  LV_CUDA(cudaMalloc(&c->d_ksk, (size_t)kBig * kKsLevel * (n + 1) * sizeof(uint64_t)));
-  keygen_ksk_kernel<<<kBig * kKsLevel, 256, 0, c->stream>>>(c->seed, n, c->p.lwe_noise_log2,
-                                                            c->d_sk_small, c->d_sk_glwe, c->d_ksk);
-  LV_CUDA(cudaGetLastError());
   LV_CUDA(cudaMalloc(&c->d_ksk_bias, (size_t)(n + 1) * sizeof(uint64_t)));
   ksk_bias_kernel<<<(n + 1 + 127) / 128, 128, 0, c->stream>>>(c->d_ksk, n, c->d_ksk_bias);
   LV_CUDA(cudaGetLastError());
-  {
-    const uint32_t rows = ks_tc_ntiles(n) * 32 * 8;  // limb rows, zero-padded past n
-    LV_CUDA(cudaMalloc(&c->d_ksk_bt, (size_t)rows * kBig * kKsLevel));
-    ksk_limbs_kernel<<<dim3((kBig * kKsLevel + 255) / 256, rows / 8), 256, 0, c->stream>>>(
-        c->d_ksk, n, c->d_ksk_bt);
-    LV_CUDA(cudaGetLastError());
-    c->ks_tma = !std::getenv("LVB_KS_NO_TMA") && make_ks_tensor_map(&c->ksk_map, c->d_ksk_bt, rows, 256);
-  }
-  uint64_t* d_bsk = nullptr;
-  LV_CUDA(cudaMalloc(&d_bsk, (size_t)n * kRows * (kK + 1) * kN * sizeof(uint64_t)));
-  keygen_bsk_kernel<<<n * kRows, 256, 0, c->stream>>>(c->seed, c->p.glwe_noise_log2, c->d_sk_small,
-                                                      c->d_sk_glwe, d_bsk);
+  const uint32_t rows = ks_tc_ntiles(n) * 32 * 8;  // limb rows, zero-padded past n
+  LV_CUDA(cudaMalloc(&c->d_ksk_bt, (size_t)rows * kBig * kKsLevel));
+  ksk_limbs_kernel<<<dim3((kBig * kKsLevel + 255) / 256, rows / 8), 256, 0, c->stream>>>(
+      c->d_ksk, n, c->d_ksk_bt);
   LV_CUDA(cudaGetLastError());
+  c->ks_tma = !std::getenv("LVB_KS_NO_TMA") && make_ks_tensor_map(&c->ksk_map, c->d_ksk_bt, rows, 256);
+}
+
+// Standard-domain BSK (device, [i][row][poly][N] u64) generated from the seed.
+static void gen_bsk(lv_ctx* c, uint64_t* d_bsk) {
+  keygen_bsk_kernel<<<c->p.n * kRows, 256, 0, c->stream>>>(c->seed, c->p.glwe_noise_log2,
+                                                            c->d_sk_small, c->d_sk_glwe, d_bsk);
+  LV_CUDA(cudaGetLastError());
+}
+
+// The resident Fourier BSK (c->d_bskf) from a standard-domain BSK.
+static void derive_bsk(lv_ctx* c, const uint64_t* d_bsk) {
+  const uint32_t n = c->p.n;
   const bool exact = c->p.exact_mask_product != 0;
   const uint32_t nouts = exact ? 3 : 2;  // spectra per GGSW row: [mask, body] or [H, Lo, body]
   LV_CUDA(cudaMalloc(&c->d_bskf, (size_t)n * 8 * kRows * nouts * 128 * sizeof(double2)));
@@ -456,10 +464,42 @@ static void keygen(lv_ctx* c) {
                                                                 d_tw_dd, d_twist_dd, c->d_bskf);
   LV_CUDA(cudaGetLastError());
   LV_CUDA(cudaStreamSynchronize(c->stream));
-  LV_CUDA(cudaFree(d_bsk));
   LV_CUDA(cudaFree(d_tw_dd));
   LV_CUDA(cudaFree(d_twist_dd));
   if (d_split) LV_CUDA(cudaFree(d_split));
+}
+
+// Secret keys, KSK and BSK from the seed (a client context).
+static void keygen(lv_ctx* c) {
+  const uint32_t n = c->p.n;
+  LV_CUDA(cudaMalloc(&c->d_sk_small, n));
+  LV_CUDA(cudaMalloc(&c->d_sk_glwe, kBig));
+  keygen_secret_kernel<<<(std::max(n, kBig) + 255) / 256, 256, 0, c->stream>>>(c->seed, n, c->d_sk_small,
+                                                                              c->d_sk_glwe);
+  LV_CUDA(cudaGetLastError());
+  LV_CUDA(cudaMalloc(&c->d_ksk, ksk_words(n) * sizeof(uint64_t)));
+  keygen_ksk_kernel<<<kBig * kKsLevel, 256, 0, c->stream>>>(c->seed, n, c->p.lwe_noise_log2,
+                                                            c->d_sk_small, c->d_sk_glwe, c->d_ksk);
+  LV_CUDA(cudaGetLastError());
+  derive_ksk(c);
+  uint64_t* d_bsk = nullptr;
+  LV_CUDA(cudaMalloc(&d_bsk, bsk_words(n) * sizeof(uint64_t)));
+  gen_bsk(c, d_bsk);
+  derive_bsk(c, d_bsk);
+  LV_CUDA(cudaFree(d_bsk));
+}
+
+// Evaluation keys received from a client (a server context: no secret key).
+static void load_eval_keys(lv_ctx* c, const uint64_t* bsk, const uint64_t* ksk) {
+  const uint32_t n = c->p.n;
+  LV_CUDA(cudaMalloc(&c->d_ksk, ksk_words(n) * sizeof(uint64_t)));
+  LV_CUDA(cudaMemcpy(c->d_ksk, ksk, ksk_words(n) * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  derive_ksk(c);
+  uint64_t* d_bsk = nullptr;
+  LV_CUDA(cudaMalloc(&d_bsk, bsk_words(n) * sizeof(uint64_t)));
+  LV_CUDA(cudaMemcpy(d_bsk, bsk, bsk_words(n) * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  derive_bsk(c, d_bsk);
+  LV_CUDA(cudaFree(d_bsk));
 }
 
 std::array<int32_t, 16> eq_lut_entries(int scale) {  // equality.cpp:31-36
@@ -527,7 +567,8 @@ int lv_lut_table(int32_t which, int32_t* out16) {
   });
 }
 
-int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
+static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bsk,
+                      const uint64_t* ksk, uint64_t key_id, lv_ctx** out) {
   return guard([&] {
     lv_params p;
     if (params)
@@ -549,6 +590,7 @@ int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
     try {
       c->p = p;
       c->seed = seed;
+      c->key_id = key_id;
       LV_CUDA(cudaGetDevice(&c->device));
       LV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       LV_CUDA(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
@@ -581,7 +623,10 @@ int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
         c->br_slots = (uint32_t)(sms * std::max(per_sm, 1));
       }
       build_tables(c);
-      keygen(c);
+      if (bsk)
+        load_eval_keys(c, bsk, ksk);
+      else
+        keygen(c);
       c->min_lut[0] = lut_id(c, min_lut_entries(false));
       c->min_lut[1] = lut_id(c, min_lut_entries(true));
       std::array<int32_t, 16> id{};
@@ -593,6 +638,44 @@ int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
       throw;
     }
     *out = c;
+  });
+}
+
+int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
+  return create_ctx(params, seed, nullptr, nullptr, seed, out);
+}
+
+int lv_ctx_create_eval(const lv_params* params, const uint64_t* bsk, const uint64_t* ksk,
+                       uint64_t key_id, lv_ctx** out) {
+  if (!bsk || !ksk)
+    return guard([] { throw Error(LV_ERR_INVALID_PARAMS, "evaluation keys missing"); });
+  return create_ctx(params, 0, bsk, ksk, key_id, out);
+}
+
+int lv_keys_size(const lv_params* params, uint64_t* bsk_count, uint64_t* ksk_count) {
+  return guard([&] {
+    if (params->n < 1 || params->n > 4096) throw Error(LV_ERR_INVALID_PARAMS, "n out of range");
+    *bsk_count = bsk_words(params->n);
+    *ksk_count = ksk_words(params->n);
+  });
+}
+
+int lv_keys_export(lv_ctx* c, uint64_t* bsk, uint64_t* ksk, uint64_t* key_id) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    need_secret(c);
+    const uint32_t n = c->p.n;
+    if (ksk) LV_CUDA(cudaMemcpy(ksk, c->d_ksk, ksk_words(n) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    if (bsk) {  // regenerated from the seed: the context keeps only the Fourier form
+      uint64_t* d_bsk = nullptr;
+      LV_CUDA(cudaMalloc(&d_bsk, bsk_words(n) * sizeof(uint64_t)));
+      gen_bsk(c, d_bsk);
+      LV_CUDA(cudaMemcpyAsync(bsk, d_bsk, bsk_words(n) * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                              c->stream));
+      LV_CUDA(cudaStreamSynchronize(c->stream));
+      LV_CUDA(cudaFree(d_bsk));
+    }
+    if (key_id) *key_id = c->key_id;
   });
 }
 
@@ -627,6 +710,7 @@ int lv_get_params(lv_ctx* c, lv_params* out) {
 int lv_encrypt(lv_ctx* c, const int32_t* values, size_t count, lv_ct* out) {
   return guard([&] {
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    need_secret(c);
     for (size_t i = 0; i < count; ++i) check_plaintext(values[i]);
     std::vector<lv_ct> s = pool_alloc(c, count);
     encrypt_into(c, values, s, false);
@@ -752,12 +836,14 @@ int lv_refresh_batch(lv_ctx* c, const lv_ct* in, size_t count, lv_ct* out) {
   return guard([&] {
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     check_handles(c, in, count);
-    std::vector<uint64_t> ph = phases(c, in, count);
-    for (size_t i = 0; i < count; ++i) {  // backend.cpp:72-80
-      const int32_t v = decode(ph[i]);
-      if (v >= 16)
-        throw Error(LV_ERR_VALUE_OUTSIDE_LUT_HALF,
-                    "refresh needs a value in [0,16), got " + std::to_string(v));
+    if (c->d_sk_glwe) {  // backend.cpp:72-80; a server (no secret key) cannot check
+      std::vector<uint64_t> ph = phases(c, in, count);
+      for (size_t i = 0; i < count; ++i) {
+        const int32_t v = decode(ph[i]);
+        if (v >= 16)
+          throw Error(LV_ERR_VALUE_OUTSIDE_LUT_HALF,
+                      "refresh needs a value in [0,16), got " + std::to_string(v));
+      }
     }
     std::vector<uint32_t> luts(count, c->identity_lut);
     pbs_batch(c, in, luts.data(), count, out);
@@ -903,6 +989,7 @@ int lv_pbs_batch_host(lv_ctx* c, const uint64_t* in, const uint32_t* luts, size_
 int lv_debug_keys(lv_ctx* c, uint8_t* sk_small, uint8_t* sk_glwe, uint64_t* ksk, double* bskf_nat) {
   return guard([&] {
     std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (sk_small || sk_glwe) need_secret(c);
     const uint32_t n = c->p.n;
     if (sk_small) LV_CUDA(cudaMemcpy(sk_small, c->d_sk_small, n, cudaMemcpyDeviceToHost));
     if (sk_glwe) LV_CUDA(cudaMemcpy(sk_glwe, c->d_sk_glwe, kBig, cudaMemcpyDeviceToHost));

@@ -65,6 +65,7 @@ struct lv_eqtable {
 struct lv_ctx {
   lv_params p{};
   uint64_t seed = 0;
+  uint64_t key_id = 0;  // key-set fingerprint (the seed of the context that generated the keys)
   cudaStream_t stream = nullptr;
   cudaStream_t copy_out = nullptr;  // lv_pbs_batch_host: chunk downloads behind the compute
   int device = 0;

@@ -588,7 +588,7 @@ __global__ void encrypt_kernel(EncArgs a) {
   for (uint32_t j = threadIdx.x; j < kBig; j += blockDim.x) {
     const uint64_t m = a.trivial ? 0 : philox_u64(a.seed, kDomEncMask, ctr * kBig + j);
     out[j] = m;
-    if (a.sk_glwe[j]) s += m;
+    if (!a.trivial && a.sk_glwe[j]) s += m;  // trivials: no key (evaluation contexts)
   }
   red[threadIdx.x] = s;
   __syncthreads();

@@ -532,7 +532,7 @@ int lv_eq_table_serialize(lv_ctx* c, const lv_eqtable* t, const uint8_t* meta, u
     put<uint32_t>(b, c->p.n);
     put<uint32_t>(b, c->p.N);
     put<uint32_t>(b, c->p.k);
-    put<uint64_t>(b, c->seed);
+    put<uint64_t>(b, c->key_id);
     put<uint64_t>(b, t->length);
     put<uint32_t>(b, (uint32_t)t->rows.size());
     std::vector<uint64_t> rows(t->length * (kBig + 1));
@@ -584,7 +584,7 @@ int lv_eq_table_deserialize(lv_ctx* c, const uint8_t* buf, uint64_t len, lv_eqta
     pos += ml;
     const uint32_t n = get32(), N = get32(), k = get32();
     const uint64_t seed = get64();
-    if (n != c->p.n || N != c->p.N || k != c->p.k || seed != c->seed)
+    if (n != c->p.n || N != c->p.N || k != c->p.k || seed != c->key_id)
       throw Error(LV_ERR_INVALID_PARAMS, "table was encrypted under a different keyset");
     const uint64_t length = get64();
     const uint32_t nrows = get32();

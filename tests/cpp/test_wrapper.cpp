@@ -106,6 +106,28 @@ int main() {
     CHECK(scan[0].counters.kernel_pbs == 56);
     delete t;
   }
+  {
+    // client / server split: the server evaluates with exported keys only
+    GpuBackend client(4000.0, 7);
+    const GpuBackend::EvalKeys keys = client.export_keys();
+    CHECK(keys.key_id == 7);
+    std::unique_ptr<GpuBackend> server = GpuBackend::evaluation(keys);
+    CHECK(throws<InvalidParams>([&] { server->encrypt(1); }));
+    const std::vector<Ct> xs = client.encrypt(std::vector<int32_t>{3, 12, 20});
+    std::vector<uint64_t> rows(xs.size() * 2049), back(xs.size() * 2049);
+    check(lv_export(client.raw(), xs.data(), xs.size(), rows.data()));
+    std::vector<Ct> on_server(xs.size()), out(xs.size());
+    check(lv_import(server->raw(), rows.data(), rows.size() / 2049, on_server.data()));
+    const Lut16 minus4 = {12, 13, 14, 15, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11};  // x - 4
+    const uint32_t id = server->lut(minus4);
+    std::vector<uint32_t> ids(xs.size(), id);
+    check(lv_pbs_batch(server->raw(), on_server.data(), ids.data(), xs.size(), out.data()));
+    check(lv_export(server->raw(), out.data(), out.size(), back.data()));
+    std::vector<Ct> mine(xs.size());
+    check(lv_import(client.raw(), back.data(), xs.size(), mine.data()));
+    const std::vector<int32_t> got = client.decrypt(mine);
+    CHECK(got.size() == 3 && got[0] == 15 && got[1] == 8 && got[2] == 0);  // negacyclic_eval(x - 4)
+  }
   std::printf("%s: %d failures\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail;
 }
