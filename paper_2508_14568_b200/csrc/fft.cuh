@@ -54,20 +54,31 @@ constexpr int kXchgBufs = kSplitXchg ? 1 : 2;
 #define LVB_TW_EARLY 1  // twiddles requested before the exchange that precedes their group
 #endif
 
-// Moves X from layout wr(r) to layout rd(r) (element indices x); the caller
-// guarantees the buffer is free on entry.
-template <int P, typename WR, typename RD>
+// Moves X from layout wr(r) to layout rd(r) (element indices x).
+// kWarp: both layouts keep warp w inside the 256-point block w (x >> 8 = w;
+// swz() preserves it), so only this warp reads or writes that part of the
+// buffer and __syncwarp orders the exchange. Otherwise the exchange crosses
+// warps: the caller guarantees no other warp still reads the addresses
+// written (this warp's own earlier reads are ordered here).
+template <int P, bool kWarp = false, typename WR, typename RD>
 __device__ __forceinline__ void xchg(double2 (&X)[P][8], double2* buf, WR wr, RD rd) {
 #ifdef LVB_ABL_XCHG  // timing ablation only: results are wrong
   __syncthreads();
   return;
 #endif
+  auto sync = [] {
+    if constexpr (kWarp)
+      __syncwarp();
+    else
+      __syncthreads();
+  };
+  __syncwarp();
   if constexpr (!kSplitXchg || P == 1) {
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; ++r) buf[p * kM + swz(wr(r))] = X[p][r];
-    __syncthreads();
+    sync();
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -75,10 +86,10 @@ __device__ __forceinline__ void xchg(double2 (&X)[P][8], double2* buf, WR wr, RD
   } else {
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      if (p) __syncthreads();
+      if (p) sync();
 #pragma unroll
       for (int r = 0; r < 8; ++r) buf[swz(wr(r))] = X[p][r];
-      __syncthreads();
+      sync();
 #pragma unroll
       for (int r = 0; r < 8; ++r) X[p][r] = buf[swz(rd(r))];
     }
@@ -258,10 +269,10 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
 #pragma unroll
       for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 6, m + 1, v0 + 2 * r);
 #endif
-    __syncthreads();
+    // B and C both keep warp w in block w (x >> 8 = t >> 5): warp-local
     const uint32_t c = t >> 1, v = t & 1;
-    xchg<P>(X, buf, [&](int r) { return 128 * b + u + 16 * r; },
-            [&](int r) { return 16 * c + v + 2 * r; });
+    xchg<P, true>(X, buf, [&](int r) { return 128 * b + u + 16 * r; },
+                  [&](int r) { return 16 * c + v + 2 * r; });
     hook();
 #if LVB_TW_EARLY
     // group C continues in this scope (w already holds its twiddles)
@@ -310,8 +321,9 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
 // ------------------------------------------------------------- inverse
 // X[p][r] on entry: spectrum bins 8t + r. On exit: layout A (x = t + 128 r),
 // the layout fft_forward's input uses, so each thread owns the same
-// accumulator coefficients in both halves of a CMUX. Buffer reuse is
-// guarded by the caller's __syncthreads before entry.
+// accumulator coefficients in both halves of a CMUX. The first exchange is
+// warp-local, so the caller only has to order this warp's earlier buffer
+// reads (__syncwarp).
 template <int P>
 __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
                                               const double2* __restrict__ tw, uint32_t t) {
@@ -335,7 +347,9 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
 #pragma unroll
     for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 4, m + 1, u + 8 * r);
 #endif
-  xchg<P>(X, buf, [&](int r) { return 8 * t + r; }, [&](int r) { return 64 * b + u + 8 * r; });
+  // bins 8t + r and B' both keep warp w in block w: warp-local
+  xchg<P, true>(X, buf, [&](int r) { return 8 * t + r; },
+                [&](int r) { return 64 * b + u + 8 * r; });
   {
     // stage 6, radix-4 (5,4) with j = u + 8 r
 #if !LVB_TW_EARLY
@@ -389,7 +403,8 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
 #pragma unroll
     for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 0, m + 1, t + 128 * r);
 #endif
-  __syncthreads();
+  // B' -> A crosses warps; B' writes stay in this warp's block, which other
+  // warps stopped reading at the (warp-local) exchange above
   xchg<P>(
       X, buf,
       [&](int r) { return 64 * (b & ~1u) + u + 8 * ((r & 3) + 4 * odd) + 64 * (r >> 2); },

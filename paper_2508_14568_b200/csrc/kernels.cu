@@ -208,7 +208,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         Z[1][q] = mac2(d0, l0, d1, l1);
         Z[2][q] = mac2(d1, b1, d0, b0);  // body output: row 1 first
       }
-      __syncthreads();  // forward's last buffer reads precede the inverse's writes
+      __syncwarp();  // the forward's last (warp-local) buffer reads precede the inverse's
       fft_inverse_a<3>(Z, buf, tw, t);
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
@@ -237,7 +237,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         X[0][q] = mac2(d0, b00, d1, b10);
         X[1][q] = mac2(d1, b11, d0, b01);  // output o: row o first
       }
-      __syncthreads();  // forward's last buffer reads precede the inverse's writes
+      __syncwarp();  // the forward's last (warp-local) buffer reads precede the inverse's
       fft_inverse_a<2>(X, buf, tw, t);
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
@@ -426,7 +426,7 @@ blind_rotate_pair_kernel(BrArgs a) {
     }
     uses += parity;  // each buffer's barrier completes once per two CMUXes
     parity ^= 1u;
-    __syncthreads();  // forward's last buffer reads precede the inverse's writes
+    __syncwarp();  // the forward's last (warp-local) buffer reads precede the inverse's
     fft_inverse_a<1>(X, buf, tw, t);  // its barriers also order the rotated reads before the update
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
