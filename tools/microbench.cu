@@ -131,7 +131,8 @@ __global__ void k_tmem(unsigned* out, int iters, int do_load) {
             "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
           : "r"(base + col));
       asm volatile("tcgen05.wait::ld.sync.aligned;");
-      acc += r[it & 31];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) acc += r[k];  // static indices (no local-memory copy)
     } else {
       asm volatile(
           "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
@@ -141,7 +142,8 @@ __global__ void k_tmem(unsigned* out, int iters, int do_load) {
           "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
           "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
           "r"(r[29]), "r"(r[30]), "r"(r[31]));
-      r[it & 31] += 1;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) r[k] += 1;
     }
   }
   asm volatile("tcgen05.wait::st.sync.aligned;");
