@@ -448,25 +448,19 @@ static void derive_bsk(lv_ctx* c, const uint64_t* d_bsk) {
       twist_dd[j] = split(cosl(ang), sinl(ang));
     }
   }
-  double4 *d_tw_dd = nullptr, *d_twist_dd = nullptr;
-  LV_CUDA(cudaMalloc(&d_tw_dd, tw_dd.size() * sizeof(double4)));
-  LV_CUDA(cudaMalloc(&d_twist_dd, twist_dd.size() * sizeof(double4)));
-  LV_CUDA(cudaMemcpy(d_tw_dd, tw_dd.data(), tw_dd.size() * sizeof(double4), cudaMemcpyHostToDevice));
-  LV_CUDA(cudaMemcpy(d_twist_dd, twist_dd.data(), twist_dd.size() * sizeof(double4),
+  DevTemp<double4> d_tw_dd(tw_dd.size()), d_twist_dd(twist_dd.size());
+  LV_CUDA(cudaMemcpy(d_tw_dd.p, tw_dd.data(), tw_dd.size() * sizeof(double4), cudaMemcpyHostToDevice));
+  LV_CUDA(cudaMemcpy(d_twist_dd.p, twist_dd.data(), twist_dd.size() * sizeof(double4),
                      cudaMemcpyHostToDevice));
-  uint64_t* d_split = nullptr;
+  DevTemp<uint64_t> d_split(exact ? (size_t)n * kRows * 3 * kN : 0);
   if (exact) {
-    LV_CUDA(cudaMalloc(&d_split, (size_t)n * kRows * 3 * kN * sizeof(uint64_t)));
-    bsk_split_kernel<<<n * kRows, 256, 0, c->stream>>>(d_bsk, d_split);
+    bsk_split_kernel<<<n * kRows, 256, 0, c->stream>>>(d_bsk, d_split.p);
     LV_CUDA(cudaGetLastError());
   }
-  bsk_fourier_kernel<<<n * kRows * nouts, 512, 0, c->stream>>>(exact ? d_split : d_bsk, nouts,
-                                                                d_tw_dd, d_twist_dd, c->d_bskf);
+  bsk_fourier_kernel<<<n * kRows * nouts, 512, 0, c->stream>>>(exact ? d_split.p : d_bsk, nouts,
+                                                                d_tw_dd.p, d_twist_dd.p, c->d_bskf);
   LV_CUDA(cudaGetLastError());
   LV_CUDA(cudaStreamSynchronize(c->stream));
-  LV_CUDA(cudaFree(d_tw_dd));
-  LV_CUDA(cudaFree(d_twist_dd));
-  if (d_split) LV_CUDA(cudaFree(d_split));
 }
 
 // Secret keys, KSK and BSK from the seed (a client context).
@@ -482,11 +476,9 @@ static void keygen(lv_ctx* c) {
                                                             c->d_sk_small, c->d_sk_glwe, c->d_ksk);
   LV_CUDA(cudaGetLastError());
   derive_ksk(c);
-  uint64_t* d_bsk = nullptr;
-  LV_CUDA(cudaMalloc(&d_bsk, bsk_words(n) * sizeof(uint64_t)));
-  gen_bsk(c, d_bsk);
-  derive_bsk(c, d_bsk);
-  LV_CUDA(cudaFree(d_bsk));
+  DevTemp<uint64_t> d_bsk(bsk_words(n));
+  gen_bsk(c, d_bsk.p);
+  derive_bsk(c, d_bsk.p);
 }
 
 // Evaluation keys received from a client (a server context: no secret key).
@@ -495,11 +487,9 @@ static void load_eval_keys(lv_ctx* c, const uint64_t* bsk, const uint64_t* ksk) 
   LV_CUDA(cudaMalloc(&c->d_ksk, ksk_words(n) * sizeof(uint64_t)));
   LV_CUDA(cudaMemcpy(c->d_ksk, ksk, ksk_words(n) * sizeof(uint64_t), cudaMemcpyHostToDevice));
   derive_ksk(c);
-  uint64_t* d_bsk = nullptr;
-  LV_CUDA(cudaMalloc(&d_bsk, bsk_words(n) * sizeof(uint64_t)));
-  LV_CUDA(cudaMemcpy(d_bsk, bsk, bsk_words(n) * sizeof(uint64_t), cudaMemcpyHostToDevice));
-  derive_bsk(c, d_bsk);
-  LV_CUDA(cudaFree(d_bsk));
+  DevTemp<uint64_t> d_bsk(bsk_words(n));
+  LV_CUDA(cudaMemcpy(d_bsk.p, bsk, bsk_words(n) * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  derive_bsk(c, d_bsk.p);
 }
 
 std::array<int32_t, 16> eq_lut_entries(int scale) {  // equality.cpp:31-36
@@ -667,13 +657,11 @@ int lv_keys_export(lv_ctx* c, uint64_t* bsk, uint64_t* ksk, uint64_t* key_id) {
     const uint32_t n = c->p.n;
     if (ksk) LV_CUDA(cudaMemcpy(ksk, c->d_ksk, ksk_words(n) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     if (bsk) {  // regenerated from the seed: the context keeps only the Fourier form
-      uint64_t* d_bsk = nullptr;
-      LV_CUDA(cudaMalloc(&d_bsk, bsk_words(n) * sizeof(uint64_t)));
-      gen_bsk(c, d_bsk);
-      LV_CUDA(cudaMemcpyAsync(bsk, d_bsk, bsk_words(n) * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+      DevTemp<uint64_t> d_bsk(bsk_words(n));
+      gen_bsk(c, d_bsk.p);
+      LV_CUDA(cudaMemcpyAsync(bsk, d_bsk.p, bsk_words(n) * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                               c->stream));
       LV_CUDA(cudaStreamSynchronize(c->stream));
-      LV_CUDA(cudaFree(d_bsk));
     }
     if (key_id) *key_id = c->key_id;
   });
@@ -961,11 +949,10 @@ int lv_pbs_batch_host(lv_ctx* c, const uint64_t* in, const uint32_t* luts, size_
       const size_t nchunks = (count + chunk - 1) / chunk;
       uint32_t* done = c->u32b.get(nchunks);
       LV_CUDA(cudaMemsetAsync(done, 0, nchunks * 4, c->stream));
-      cudaEvent_t zeroed;
-      LV_CUDA(cudaEventCreateWithFlags(&zeroed, cudaEventDisableTiming));
-      LV_CUDA(cudaEventRecord(zeroed, c->stream));
+      Event zeroed(cudaEventDisableTiming);
+      LV_CUDA(cudaEventRecord(zeroed.e, c->stream));
       // the copy stream must not see the previous call's counters
-      LV_CUDA(cudaStreamWaitEvent(c->copy_out, zeroed, 0));
+      LV_CUDA(cudaStreamWaitEvent(c->copy_out, zeroed.e, 0));
       launch_pbs_dev(c, dd, dl, dout, (uint32_t)count, nullptr, done, (uint32_t)chunk);
       for (size_t k = 0; k < nchunks; ++k) {
         const size_t off = k * chunk, m = std::min(chunk, count - off);
@@ -978,7 +965,6 @@ int lv_pbs_batch_host(lv_ctx* c, const uint64_t* in, const uint32_t* luts, size_
       }
       LV_CUDA(cudaStreamSynchronize(c->copy_out));
       LV_CUDA(cudaStreamSynchronize(c->stream));
-      cudaEventDestroy(zeroed);
     }
     pool_free(c, s.data(), count);
     c->pbs_count += count;
@@ -1092,29 +1078,23 @@ int lv_debug_fft(lv_ctx* c, const int64_t* poly, double* spec, uint64_t* roundtr
 
 int lv_bench_fp64_peak(float* tflops) {
   return guard([&] {
-    double* d = nullptr;
-    LV_CUDA(cudaMalloc(&d, 8));
+    DevTemp<double> d(1);
     int sms = 0, dev = 0;
     LV_CUDA(cudaGetDevice(&dev));
     LV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int blocks = sms * 8, threads = 256, iters = 8192;
-    cudaEvent_t e0, e1;
-    LV_CUDA(cudaEventCreate(&e0));
-    LV_CUDA(cudaEventCreate(&e1));
+    Event e0, e1;
     float best = 0;
     for (int rep = 0; rep < 4; ++rep) {
-      LV_CUDA(cudaEventRecord(e0));
-      fp64_peak_kernel<<<blocks, threads>>>(d, iters, 1.0 + rep);
-      LV_CUDA(cudaEventRecord(e1));
-      LV_CUDA(cudaEventSynchronize(e1));
+      LV_CUDA(cudaEventRecord(e0.e));
+      fp64_peak_kernel<<<blocks, threads>>>(d.p, iters, 1.0 + rep);
+      LV_CUDA(cudaEventRecord(e1.e));
+      LV_CUDA(cudaEventSynchronize(e1.e));
       float ms = 0;
-      LV_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      LV_CUDA(cudaEventElapsedTime(&ms, e0.e, e1.e));
       const double flops = 2.0 * 8 * (double)iters * blocks * threads;
       best = std::max(best, (float)(flops / (ms * 1e-3) / 1e12));
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaFree(d);
     *tflops = best;
   });
 }
@@ -1137,30 +1117,22 @@ int lv_bench_pbs(lv_ctx* c, const lv_ct* in, const uint32_t* luts, size_t count,
     LV_CUDA(cudaMemcpyAsync(dd, d.data(), count * sizeof(LinDesc), cudaMemcpyHostToDevice, c->stream));
     LV_CUDA(cudaMemcpyAsync(dl, luts, count * 4, cudaMemcpyHostToDevice, c->stream));
     LV_CUDA(cudaMemcpyAsync(dout, o.data(), count * sizeof(BrOut), cudaMemcpyHostToDevice, c->stream));
-    cudaEvent_t e0, e1, e2;
-    LV_CUDA(cudaEventCreate(&e0));
-    LV_CUDA(cudaEventCreate(&e1));
-    LV_CUDA(cudaEventCreate(&e2));
-    uint4* flush = nullptr;
-    if (flush_bytes) LV_CUDA(cudaMalloc(&flush, flush_bytes));
+    Event e0, e1, e2;
+    DevTemp<uint4> flush(flush_bytes / 16);
     for (int it = 0; it < iters; ++it) {
-      if (flush) flush_kernel<<<1184, 256, 0, c->stream>>>(flush, flush_bytes / 16);
-      LV_CUDA(cudaEventRecord(e0, c->stream));
-      launch_pbs_dev(c, dd, dl, dout, (uint32_t)count, e1);
-      LV_CUDA(cudaEventRecord(e2, c->stream));
-      LV_CUDA(cudaEventSynchronize(e2));
+      if (flush_bytes) flush_kernel<<<1184, 256, 0, c->stream>>>(flush.p, flush_bytes / 16);
+      LV_CUDA(cudaEventRecord(e0.e, c->stream));
+      launch_pbs_dev(c, dd, dl, dout, (uint32_t)count, e1.e);
+      LV_CUDA(cudaEventRecord(e2.e, c->stream));
+      LV_CUDA(cudaEventSynchronize(e2.e));
       float a = 0, b = 0, s = 0;
-      LV_CUDA(cudaEventElapsedTime(&a, e0, e1));
-      LV_CUDA(cudaEventElapsedTime(&b, e1, e2));
-      LV_CUDA(cudaEventElapsedTime(&s, e0, e2));
+      LV_CUDA(cudaEventElapsedTime(&a, e0.e, e1.e));
+      LV_CUDA(cudaEventElapsedTime(&b, e1.e, e2.e));
+      LV_CUDA(cudaEventElapsedTime(&s, e0.e, e2.e));
       if (ks_ms) ks_ms[it] = a;
       if (br_ms) br_ms[it] = b;
       if (step_ms) step_ms[it] = s;
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaEventDestroy(e2);
-    if (flush) cudaFree(flush);
     pool_free(c, dst.data(), count);
     c->pbs_count += (uint64_t)count * iters;
   });

@@ -48,6 +48,28 @@ struct DevBuf {  // grow-only device scratch buffer
   }
 };
 
+// Scoped device allocation / event (freed on every exit path, exceptions
+// included).
+template <typename T>
+struct DevTemp {
+  T* p = nullptr;
+  explicit DevTemp(size_t n) { LV_CUDA(cudaMalloc(&p, n * sizeof(T))); }
+  ~DevTemp() {
+    if (p) cudaFree(p);
+  }
+  DevTemp(const DevTemp&) = delete;
+  DevTemp& operator=(const DevTemp&) = delete;
+};
+struct Event {
+  cudaEvent_t e = nullptr;
+  explicit Event(unsigned flags = cudaEventDefault) { LV_CUDA(cudaEventCreateWithFlags(&e, flags)); }
+  ~Event() {
+    if (e) cudaEventDestroy(e);
+  }
+  Event(const Event&) = delete;
+  Event& operator=(const Event&) = delete;
+};
+
 // Epilogue of one blind-rotation item (see BrOut in kernels.cuh).
 struct PbsItem {
   LinDesc in;        // key-switch prologue
