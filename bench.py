@@ -375,6 +375,15 @@ def main():
                                               f"in {dt:.1f}s (oracle/tfhe_oracle.c), correct={ok}"}
         except Exception as e:
             line["cpu_baseline"] = {"error": repr(e)}
+        # DP cells/s of the CPU port at the same bootstraps per cell (the
+        # port's PBS rate is what bounds it; its linear ops are negligible)
+        cpu = line.get("cpu_baseline", {}).get("value")
+        if cpu and isinstance(line.get("dp_cells"), dict):
+            for name, d in line["dp_cells"].items():
+                if isinstance(d, dict) and d.get("cells") and (d.get("pbs") or d.get("table_pbs") is not None):
+                    pbs = d.get("pbs") or (d["cells"] + (d.get("table_pbs") or 0))
+                    d["cpu_port_cells_per_s"] = cpu * d["cells"] / pbs
+                    d["vs_cpu_port"] = d["cells_per_s"] / d["cpu_port_cells_per_s"]
         try:  # the exact-mask-product keys: same workload, 1.0x exact noise
             p = L.default_params()
             p.exact_mask_product = 1
