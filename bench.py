@@ -36,6 +36,8 @@ sys.path.insert(0, ROOT)
 BATCH = 4096
 FLOP_PER_PBS = 209.0e6  # 3520 transforms x 5(N/2)log2(N/2) + MAC, FP64
 BSK_BYTES = 880 * 2 * 2 * 1024 * 16  # Fourier BSK streamed once per PBS by each item
+KSK_LIMB_BYTES = 2048 * 5 * 896 * 8  # tensor-core KSK operand (byte limbs, n+1 padded to 896)
+KS_OPS_PER_PBS = 2 * 10240 * 881 * 8  # u8 x u8 MACs of the 8 limb GEMMs (2 ops each)
 L2_FLUSH = 256 << 20
 
 
@@ -350,7 +352,13 @@ def main():
                              "peak = DFMA throughput measured on this GPU by lv_bench_fp64_peak "
                              "(MEASURED_PEAKS.json has no FP64 entry)",
                      "hbm_view": {"bsk_bytes_per_pbs": BSK_BYTES,
-                                  "achieved_gbs": BSK_BYTES * BATCH / (br_ms / 1e3) / 1e9}},
+                                  "achieved_gbs": BSK_BYTES * BATCH / (br_ms / 1e3) / 1e9},
+                     # the key switch (tcgen05 int8 GEMM): KSK byte limbs read
+                     # from HBM once per launch, 72 MOP int8 per PBS
+                     "ks_view": {"kernel_ms": ks_ms, "ksk_limb_bytes": KSK_LIMB_BYTES,
+                                 "ksk_hbm_gbs": KSK_LIMB_BYTES / (ks_ms / 1e3) / 1e9,
+                                 "int8_tops": KS_OPS_PER_PBS * BATCH / (ks_ms / 1e3) / 1e12,
+                                 "int8_dense_peak_tops": 4500.0}},
         "e2e": {"value": ws * BATCH / e2e_s, "unit": "PBS/s",
                 "h2d_bytes_per_step": int(rows.nbytes), "d2h_bytes_per_step": int(rows.nbytes),
                 "correct": bool(e2e_ok)},
