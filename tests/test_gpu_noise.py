@@ -125,3 +125,24 @@ def test_exact_mask_product_mode():
         assert frac < 0.005, frac  # measured 2^85.8 / 2^97.9 = 2.3e-4
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("exact_mask", [0, 1])
+def test_measured_output_noise_4096(exact_mask):
+    """North-star noise criterion, measured: the output phase error of 4096
+    independent bootstraps against the exact-product model. Default keys:
+    1 + 0.19 predicted (0.91x the reference's f64-spectrum algorithm);
+    exact-mask keys: 1.0002 predicted. Sampling std error ~2.5%."""
+    p = L.default_params()
+    p.exact_mask_product = exact_mask
+    c = L.Context(seed=11, params=p)
+    try:
+        vals = [(5 * i + 3) % 16 for i in range(4096)]
+        out = c.pbs(c.encrypt(vals), L.identity_lut())
+        e = (c.phase(out) - np.asarray(vals, np.uint64) * np.uint64(1 << 59)).view(np.int64)
+        ratio = float(np.var(e.astype(np.float64))) / exact_model_var()
+        lo, hi = (1.07, 1.32) if exact_mask == 0 else (0.89, 1.11)
+        assert lo < ratio < hi, ratio
+        assert ratio < 1.1 * 1.31  # within 1.1x of the reference's algorithm
+    finally:
+        c.close()
