@@ -189,7 +189,10 @@ static void launch_keyswitch(lv_ctx* c, const LinDesc* d_desc, uint32_t count, u
 // size.
 void launch_blind_rotate(lv_ctx* c, const BrArgs& ba, uint32_t count) {
   if (!count) return;
-  if (c->p.exact_mask_product)
+  if (c->p.exact_mask_product && count <= c->br_pair_max)
+    blind_rotate_pair_exact_kernel<<<2 * count, 128, blind_rotate_pair_smem_bytes(c->p.n),
+                                     c->stream>>>(ba);
+  else if (c->p.exact_mask_product)
     blind_rotate_exact_kernel<<<count, 128, blind_rotate_smem_bytes(c->p.n, true), c->stream>>>(ba);
   else if (count <= c->br_pair_max)
     blind_rotate_pair_kernel<<<2 * count, 128, blind_rotate_pair_smem_bytes(c->p.n), c->stream>>>(ba);
@@ -595,6 +598,9 @@ static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bs
       LV_CUDA(cudaFuncSetAttribute(ks_mma_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)ks_tma_smem_bytes()));
       LV_CUDA(cudaFuncSetAttribute(blind_rotate_pair_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)blind_rotate_pair_smem_bytes(p.n)));
+      LV_CUDA(cudaFuncSetAttribute(blind_rotate_pair_exact_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)blind_rotate_pair_smem_bytes(p.n)));
       {

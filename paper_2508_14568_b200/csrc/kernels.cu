@@ -296,8 +296,12 @@ size_t blind_rotate_smem_bytes(uint32_t n, bool) {
 // results are bit-identical), then inverse-transforms and accumulates it.
 namespace cg = cooperative_groups;
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
-blind_rotate_pair_kernel(BrArgs a) {
+// kExact (exact_mask_product keys, BSK layout [i][q*6 + row*3 + (H, Lo,
+// body)][t]): the mask CTA forms the H and Lo outputs and inverts both in
+// lockstep (mask = acc + 2^43 round(H) + Lo, as blind_rotate_exact_kernel),
+// the body CTA the body output; same FMA orders as the exact kernel.
+template <bool kExact>
+__device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* acc = reinterpret_cast<uint64_t*>(smem);                    // [kN] own polynomial
   double2* buf = reinterpret_cast<double2*>(smem + kN * 8);             // [kM] FFT exchanges
@@ -365,7 +369,7 @@ blind_rotate_pair_kernel(BrArgs a) {
 
     // this CMUX's BSK row (bins 8t + q, outputs p), in flight during the forward FFT
     double2 b0[8], b1[8];
-    {
+    if constexpr (!kExact) {
       const double2* bsk = bsk_base + (size_t)i * (32 * 128);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -415,8 +419,8 @@ blind_rotate_pair_kernel(BrArgs a) {
           "r"(ph)
           : "memory");
     }
-    {
-      const double2* other_spec = spec + parity * kM;
+    const double2* other_spec = spec + parity * kM;
+    if constexpr (!kExact) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         // output p = own spectrum x B[row p][out p] + partner's x B[row 1-p][out p]
@@ -426,6 +430,50 @@ blind_rotate_pair_kernel(BrArgs a) {
     }
     uses += parity;  // each buffer's barrier completes once per two CMUXes
     parity ^= 1u;
+    if constexpr (kExact) {
+      const double2* bsk = a.bskf + (size_t)i * (8 * 6 * 128) + t;
+      if (p == 0) {  // mask: H and Lo outputs, rows in order (d0 = own spectrum)
+        double2 Z[2][8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double2* bq = bsk + q * (6 * 128);
+          const double2 d1 = other_spec[q * 128 + t];
+          Z[0][q] = mac2(X[0][q], ld_stream(bq), d1, ld_stream(bq + 384));
+          Z[1][q] = mac2(X[0][q], ld_stream(bq + 128), d1, ld_stream(bq + 512));
+        }
+        __syncwarp();  // the forward's last (warp-local) buffer reads precede the inverse's
+        fft_inverse_a<2>(Z, buf, tw, t);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const double2 ut = make_double2(tz[r].x, -tz[r].y);
+          const uint32_t x = t + 128 * r;
+          const double2 zh = cmul(Z[0][r], ut), zl = cmul(Z[1][r], ut);
+          own[2 * r] += (f64_to_torus(zh.x) << 43) + f64_to_torus(zl.x);
+          own[2 * r + 1] += (f64_to_torus(zh.y) << 43) + f64_to_torus(zl.y);
+          acc[x] = own[2 * r];
+          acc[x + kM] = own[2 * r + 1];
+        }
+      } else {  // body: row 1 (own) first, as the exact kernel
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double2* bq = bsk + q * (6 * 128);
+          X[0][q] = mac2(X[0][q], ld_stream(bq + 640), other_spec[q * 128 + t], ld_stream(bq + 256));
+        }
+        __syncwarp();
+        fft_inverse_a<1>(X, buf, tw, t);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const double2 ut = make_double2(tz[r].x, -tz[r].y);
+          const uint32_t x = t + 128 * r;
+          const double2 z = cmul(X[0][r], ut);
+          own[2 * r] += f64_to_torus(z.x);
+          own[2 * r + 1] += f64_to_torus(z.y);
+          acc[x] = own[2 * r];
+          acc[x + kM] = own[2 * r + 1];
+        }
+      }
+      continue;
+    }
     __syncwarp();  // the forward's last (warp-local) buffer reads precede the inverse's
     fft_inverse_a<1>(X, buf, tw, t);  // its barriers also order the rotated reads before the update
 #pragma unroll
@@ -451,6 +499,15 @@ blind_rotate_pair_kernel(BrArgs a) {
   for (uint32_t j = j0; j < j1; j += 128)
     br_output(o, a.pool, a.pool_stride, j, j == 0 || j == kN ? acc[0] : (uint64_t)0 - acc[kN - j]);
   signal_done(a, item);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+blind_rotate_pair_kernel(BrArgs a) {
+  blind_rotate_pair_body<false>(a);
+}
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+blind_rotate_pair_exact_kernel(BrArgs a) {
+  blind_rotate_pair_body<true>(a);
 }
 
 // acc (16 KB) + exchange buffer (16 KB) + 2 published spectra (32 KB) + ms.

@@ -109,6 +109,7 @@ __global__ void blind_rotate_kernel(BrArgs a);        // lv_params.exact_mask_pr
 __global__ void blind_rotate_exact_kernel(BrArgs a);  // lv_params.exact_mask_product = 1
 size_t blind_rotate_smem_bytes(uint32_t n, bool exact);
 __global__ void blind_rotate_pair_kernel(BrArgs a);
+__global__ void blind_rotate_pair_exact_kernel(BrArgs a);  // exact_mask_product keys
 size_t blind_rotate_pair_smem_bytes(uint32_t n);
 __global__ void keyswitch_kernel(KsArgs a);
 __global__ void linear_kernel(LinArgs a);

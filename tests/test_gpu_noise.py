@@ -96,10 +96,14 @@ def test_fft_added_phase_variance(orc):
     assert 0.12 < frac < 0.25, (frac, np.log2(vs))
 
 
-def test_exact_mask_product_mode():
+@pytest.mark.parametrize("pair_max", [0, 1 << 30])
+def test_exact_mask_product_mode(pair_max, monkeypatch):
     """lv_params.exact_mask_product = 1: bit-exact with the oracle's split
-    (H 2^43 + Lo) mask product, decrypts correctly, and the FFT's added
-    phase variance drops to a negligible fraction of the exact noise."""
+    (H 2^43 + Lo) mask product — through the single-CTA exact kernel
+    (pair_max 0) and the CTA-pair exact kernel — decrypts correctly, and the
+    FFT's added phase variance drops to a negligible fraction of the exact
+    noise."""
+    monkeypatch.setenv("LVB_BR_PAIR_MAX", str(pair_max))
     from oracle.oracle import Oracle, default_params as oracle_params
     op = oracle_params()
     op.exact_mask_product = 1
