@@ -170,3 +170,39 @@ def test_blind_rotate_variants_bit_exact(orc, pair_max, monkeypatch):
             assert np.array_equal(out[i], orc.sample_extract(want[i]))
     finally:
         c.close()
+
+
+def test_concurrent_host_threads_share_one_context(golden):
+    """backend.hpp:79-82: concurrent operations from several host threads on
+    one backend are safe and the counters add up (the context mutex
+    serialises calls onto its stream; ctypes releases the GIL)."""
+    import threading
+    c = L.Context(seed=21)
+    lut = golden["luts"]["minlut-negated"]
+    lid = c.lut(lut)
+    errors, results = [], {}
+
+    def work(k):
+        try:
+            vals = [(k * 7 + i) % 32 for i in range(50)]
+            got = []
+            for _ in range(3):
+                out = c.pbs(c.encrypt(vals), lid)
+                got.append(list(c.decrypt(out)))
+            results[k] = (vals, got)
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(6)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    try:
+        assert not errors, errors
+        for k, (vals, got) in results.items():
+            want = [L.negacyclic_eval(lut, v) for v in vals]
+            assert all(g == want for g in got), k
+        assert c.stats()["pbs_count"] == 6 * 3 * 50
+    finally:
+        c.close()
