@@ -356,11 +356,14 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
 
   // Spectra travel by st.async into the partner's inbox, each store
   // completing bytes on the partner's inbox barrier; the receiver arms its
-  // barrier (expect 16 KB) and waits with cluster-scope acquire. No cluster
-  // barrier per CMUX: the inbox alternates between two buffers by
-  // executed-CMUX parity, and a CTA overwrites a buffer only after receiving
-  // the partner's next spectrum, which the partner sends after finishing its
-  // MAC on that buffer.
+  // barrier (expect 16 KB) and waits on it. The wait is CTA-scope: the
+  // bytes land in this CTA's own shared memory and are complete when the
+  // barrier's transaction count is (a cluster-scope acquire would also
+  // invalidate L1 on every CMUX — CCTL.IVALL, 14% of the stall samples —
+  // and evict the twiddle tables). No cluster barrier per CMUX: the inbox
+  // alternates between two buffers by executed-CMUX parity, and a CTA
+  // overwrites a buffer only after receiving the partner's next spectrum,
+  // which the partner sends after finishing its MAC on that buffer.
   uint32_t parity = 0, uses = 0;
   for (uint32_t i = 0; i < n; ++i) {
     __syncthreads();  // previous update of acc visible to the rotated reads
@@ -414,7 +417,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
       asm volatile(
           "{\n\t.reg .pred P1;\n\t"
           "WAIT_INBOX:\n\t"
-          "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
           "@!P1 bra WAIT_INBOX;\n\t}" ::"r"(my_full),
           "r"(ph)
           : "memory");
