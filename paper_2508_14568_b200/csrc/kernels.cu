@@ -370,14 +370,15 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
     const uint32_t rot = ms[i];
     if (rot == 0) continue;  // uniform across the pair: both skip
 
-    // this CMUX's BSK row (bins 8t + q, outputs p), in flight during the forward FFT
-    double2 b0[8], b1[8];
+    // this CMUX's BSK row (bins 8t + q, output p), in flight during the
+    // forward FFT: row p (this CTA's own polynomial) and row 1 - p
+    double2 b_own[8], b_oth[8];
     if constexpr (!kExact) {
       const double2* bsk = bsk_base + (size_t)i * (32 * 128);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        b0[q] = ld_stream(bsk + (q * 4 + 0 + p) * 128);  // row 0, output p
-        b1[q] = ld_stream(bsk + (q * 4 + 2 + p) * 128);  // row 1, output p
+        b_own[q] = ld_stream(bsk + (q * 4 + 3 * p) * 128);      // row p, output p
+        b_oth[q] = ld_stream(bsk + (q * 4 + 2 - p) * 128);      // row 1 - p, output p
       }
     }
     double2 X[1][8];
@@ -427,8 +428,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         // output p = own spectrum x B[row p][out p] + partner's x B[row 1-p][out p]
-        X[0][q] = mac2(X[0][q], p == 0 ? b0[q] : b1[q], other_spec[q * 128 + t],
-                       p == 0 ? b1[q] : b0[q]);
+        X[0][q] = mac2(X[0][q], b_own[q], other_spec[q * 128 + t], b_oth[q]);
       }
     }
     uses += parity;  // each buffer's barrier completes once per two CMUXes
