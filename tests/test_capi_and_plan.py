@@ -34,6 +34,19 @@ def test_default_params(product_lib):
     assert p.max_variance_budget == 4000.0
 
 
+def test_evaluation_key_sizes_and_validation(product_lib):
+    """lv_keys_size (host only): BSK n*2*2*N words, KSK N*5*(n+1) words;
+    Context.evaluation rejects wrongly sized keys before touching a device."""
+    import ctypes
+    p = L.default_params()
+    nb, nk = ctypes.c_uint64(), ctypes.c_uint64()
+    assert product_lib.lv_keys_size(ctypes.byref(p), ctypes.byref(nb), ctypes.byref(nk)) == 0
+    assert (nb.value, nk.value) == (880 * 2 * 2 * 2048, 2048 * 5 * 881)
+    import numpy as np
+    with pytest.raises(L.InvalidParams):
+        L.Context.evaluation(np.zeros(7, np.uint64), np.zeros(nk.value, np.uint64), 0)
+
+
 def _band(case):
     m, n = len(case["a"]), len(case["b"])
     mode = case["mode"]
