@@ -75,30 +75,56 @@ def barrier_sync(dist):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region: NVML
+    every 10 ms (nvidia-ml-py), else nvidia-smi every 0.2 s."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, set of reason names)
         self._stop = threading.Event()
         self._th = None
 
+    def _nvml(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                    N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+            smax = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+
+            def sample():
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                return (float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)), float(smax),
+                        {n for n, b in zip(self.NAMES, bits) if r & b})
+            sample()
+            return sample
+        except Exception:
+            return None
+
+    def _smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                              "--format=csv,noheader,nounits"], capture_output=True,
+                             text=True, timeout=5).stdout.strip()
+        r = [x.strip() for x in out.split(",")]
+        return (float(r[0]), float(r[1]),
+                {n for n, v in zip(self.NAMES, r[4:8]) if v.lower() == "active"})
+
     def start(self):
+        nvml = self._nvml()
+
         def run():
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
-                                          "--format=csv,noheader,nounits"], capture_output=True,
-                                         text=True, timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([x.strip() for x in out.split(",")])
+                    self.rows.append(nvml() if nvml else self._smi())
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(0.01 if nvml else 0.2)
         self._th = threading.Thread(target=run, daemon=True)
         self._th.start()
 
@@ -108,16 +134,9 @@ class ClockSampler:
             self._th.join(timeout=6)
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for name, v in zip(names, r[4:8]):
-                if v.strip().lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+        reasons = set().union(*(r[2] for r in self.rows))
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows),
+                "sm_max_mhz": max(r[1] for r in self.rows), "reasons": sorted(reasons),
                 "samples": len(self.rows)}
 
 
