@@ -658,7 +658,7 @@ int lv_keys_size(const lv_params* params, uint64_t* bsk_count, uint64_t* ksk_cou
 
 int lv_keys_export(lv_ctx* c, uint64_t* bsk, uint64_t* ksk, uint64_t* key_id) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     need_secret(c);
     const uint32_t n = c->p.n;
     if (ksk) LV_CUDA(cudaMemcpy(ksk, c->d_ksk, ksk_words(n) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
@@ -675,6 +675,7 @@ int lv_keys_export(lv_ctx* c, uint64_t* bsk, uint64_t* ksk, uint64_t* key_id) {
 
 void lv_ctx_destroy(lv_ctx* c) {
   if (!c) return;
+  cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* p : {(void*)c->d_sk_small, (void*)c->d_sk_glwe, (void*)c->d_ksk, (void*)c->d_ksk_bias, (void*)c->d_bskf,
                   (void*)c->d_tw, (void*)c->d_twist, (void*)c->d_tp, (void*)c->d_pool})
@@ -703,7 +704,7 @@ int lv_get_params(lv_ctx* c, lv_params* out) {
 
 int lv_encrypt(lv_ctx* c, const int32_t* values, size_t count, lv_ct* out) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     need_secret(c);
     for (size_t i = 0; i < count; ++i) check_plaintext(values[i]);
     std::vector<lv_ct> s = pool_alloc(c, count);
@@ -717,7 +718,7 @@ int lv_encrypt(lv_ctx* c, const int32_t* values, size_t count, lv_ct* out) {
 
 int lv_trivial(lv_ctx* c, const int32_t* values, size_t count, lv_ct* out) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     for (size_t i = 0; i < count; ++i) check_plaintext(values[i]);
     std::vector<lv_ct> s = pool_alloc(c, count);
     encrypt_into(c, values, s, true);
@@ -727,7 +728,7 @@ int lv_trivial(lv_ctx* c, const int32_t* values, size_t count, lv_ct* out) {
 
 int lv_decrypt(lv_ctx* c, const lv_ct* cts, size_t count, int32_t* out) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     check_handles(c, cts, count);
     std::vector<uint64_t> ph = phases(c, cts, count);
     for (size_t i = 0; i < count; ++i) out[i] = decode(ph[i]);
@@ -736,7 +737,7 @@ int lv_decrypt(lv_ctx* c, const lv_ct* cts, size_t count, int32_t* out) {
 
 int lv_phase(lv_ctx* c, const lv_ct* cts, size_t count, uint64_t* out) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     check_handles(c, cts, count);
     std::vector<uint64_t> ph = phases(c, cts, count);
     std::memcpy(out, ph.data(), count * 8);
@@ -745,7 +746,7 @@ int lv_phase(lv_ctx* c, const lv_ct* cts, size_t count, uint64_t* out) {
 
 static int linear2(lv_ctx* c, const lv_ct* a, const lv_ct* b, size_t count, lv_ct* out, int sign) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     check_handles(c, a, count);
     check_handles(c, b, count);
     std::vector<lv_ct> dst = pool_alloc(c, count);
@@ -781,7 +782,7 @@ int lv_sub(lv_ctx* c, const lv_ct* a, const lv_ct* b, size_t count, lv_ct* out) 
 
 static int scalar_op(lv_ctx* c, const lv_ct* a, const int32_t* k, size_t count, lv_ct* out, bool mul) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     check_handles(c, a, count);
     std::vector<lv_ct> dst = pool_alloc(c, count);
     std::vector<LinOut> ops(count);
@@ -812,7 +813,7 @@ int lv_scalar_add(lv_ctx* c, const lv_ct* a, const int32_t* k, size_t count, lv_
 
 int lv_lut_upload(lv_ctx* c, const int32_t entries[16], uint32_t* id) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     std::array<int32_t, 16> e{};
     std::memcpy(e.data(), entries, sizeof(e));
     *id = lut_id(c, e);
@@ -821,14 +822,14 @@ int lv_lut_upload(lv_ctx* c, const int32_t entries[16], uint32_t* id) {
 
 int lv_pbs_batch(lv_ctx* c, const lv_ct* in, const uint32_t* luts, size_t count, lv_ct* out) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     pbs_batch(c, in, luts, count, out);
   });
 }
 
 int lv_refresh_batch(lv_ctx* c, const lv_ct* in, size_t count, lv_ct* out) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     check_handles(c, in, count);
     if (c->d_sk_glwe) {  // backend.cpp:72-80; a server (no secret key) cannot check
       std::vector<uint64_t> ph = phases(c, in, count);
@@ -848,7 +849,7 @@ int lv_refresh_batch(lv_ctx* c, const lv_ct* in, size_t count, lv_ct* out) {
 int lv_predict_variance(lv_ctx* c, const lv_ct* cts, const int32_t* coeffs, size_t count,
                         int64_t* out) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     check_handles(c, cts, count);
     NoiseLedger comb;
     for (size_t i = 0; i < count; ++i) comb.add_scaled(c->ledgers[cts[i]], coeffs[i]);
@@ -858,7 +859,7 @@ int lv_predict_variance(lv_ctx* c, const lv_ct* cts, const int32_t* coeffs, size
 
 int lv_ledger_variance(lv_ctx* c, const lv_ct* cts, size_t count, int64_t* out) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     check_handles(c, cts, count);
     for (size_t i = 0; i < count; ++i) out[i] = c->ledgers[cts[i]].variance();
   });
@@ -874,14 +875,14 @@ int lv_get_stats(lv_ctx* c, lv_stats* out) {
 
 int lv_release(lv_ctx* c, const lv_ct* cts, size_t count) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     pool_free(c, cts, count);
   });
 }
 
 int lv_export(lv_ctx* c, const lv_ct* cts, size_t count, uint64_t* host) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     check_handles(c, cts, count);
     download_rows(c, std::vector<lv_ct>(cts, cts + count), host);
     LV_CUDA(cudaStreamSynchronize(c->stream));
@@ -890,7 +891,7 @@ int lv_export(lv_ctx* c, const lv_ct* cts, size_t count, uint64_t* host) {
 
 int lv_import(lv_ctx* c, const uint64_t* host, size_t count, lv_ct* out) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     std::vector<lv_ct> s = pool_alloc(c, count);
     upload_rows(c, host, s);
     LV_CUDA(cudaStreamSynchronize(c->stream));
@@ -925,7 +926,7 @@ static WaitValueFn wait_value_fn() {
 int lv_pbs_batch_host(lv_ctx* c, const uint64_t* in, const uint32_t* luts, size_t count,
                       uint64_t* out) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     for (size_t i = 0; i < count; ++i)
       if (luts[i] >= c->luts.size()) throw Error(LV_ERR_INVALID_PARAMS, "unknown lut id");
     if (!count) return;
@@ -980,7 +981,7 @@ int lv_pbs_batch_host(lv_ctx* c, const uint64_t* in, const uint32_t* luts, size_
 // ------------------------------------------------------------- debug / parity
 int lv_debug_keys(lv_ctx* c, uint8_t* sk_small, uint8_t* sk_glwe, uint64_t* ksk, double* bskf_nat) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     if (sk_small || sk_glwe) need_secret(c);
     const uint32_t n = c->p.n;
     if (sk_small) LV_CUDA(cudaMemcpy(sk_small, c->d_sk_small, n, cudaMemcpyDeviceToHost));
@@ -1009,7 +1010,7 @@ int lv_debug_keys(lv_ctx* c, uint8_t* sk_small, uint8_t* sk_glwe, uint64_t* ksk,
 
 int lv_debug_keyswitch(lv_ctx* c, const uint64_t* in, size_t count, uint64_t* out_small) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     std::vector<lv_ct> s = pool_alloc(c, count);
     upload_rows(c, in, s);
     std::vector<LinDesc> d(count);
@@ -1029,7 +1030,7 @@ int lv_debug_keyswitch(lv_ctx* c, const uint64_t* in, size_t count, uint64_t* ou
 int lv_debug_blind_rotate(lv_ctx* c, const uint32_t* ms, const uint32_t* luts, size_t count,
                           uint64_t* out, uint64_t* glwe_out) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     const uint32_t row = c->p.n + 1, stride = ms_stride(c);
     std::vector<uint16_t> h((size_t)count * stride, 0);
     for (size_t i = 0; i < count; ++i)
@@ -1062,7 +1063,7 @@ int lv_debug_blind_rotate(lv_ctx* c, const uint32_t* ms, const uint32_t* luts, s
 
 int lv_debug_fft(lv_ctx* c, const int64_t* poly, double* spec, uint64_t* roundtrip) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     int64_t* dpoly = nullptr;
     double2* dspec = nullptr;
     uint64_t* drt = nullptr;
@@ -1108,7 +1109,7 @@ int lv_bench_fp64_peak(float* tflops) {
 int lv_bench_pbs(lv_ctx* c, const lv_ct* in, const uint32_t* luts, size_t count, int iters,
                  uint64_t flush_bytes, float* br_ms, float* ks_ms, float* step_ms) {
   return guard([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     check_handles(c, in, count);
     std::vector<lv_ct> dst = pool_alloc(c, count);
     std::vector<LinDesc> d(count);

@@ -143,6 +143,14 @@ struct lv_ctx {
 
 namespace lvb {
 
+// Every entry point holds the context mutex and makes the context's device
+// current on the calling thread (contexts on several GPUs, calls from any
+// host thread).
+struct CtxLock {
+  std::lock_guard<std::recursive_mutex> lk;
+  explicit CtxLock(lv_ctx* c) : lk(c->mu) { LV_CUDA(cudaSetDevice(c->device)); }
+};
+
 uint32_t ms_stride(const lv_ctx* c);
 std::vector<lv_ct> pool_alloc(lv_ctx* c, size_t count);
 void pool_free(lv_ctx* c, const lv_ct* cts, size_t count);

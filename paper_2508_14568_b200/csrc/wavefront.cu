@@ -396,7 +396,7 @@ int lv_edit_distance_ee(lv_ctx* c, const lv_ct* a, size_t m, const lv_ct* b, siz
                         uint32_t symbols, const lv_band* band, int32_t key_encoding, lv_ct* score,
                         lv_run* run) {
   return guard_wf([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     if (symbols < 1)
       throw Error(LV_ERR_INVALID_PARAMS, "equality operands must have the same nonzero symbol count");
     check_handles(c, a, m * symbols);
@@ -410,7 +410,7 @@ int lv_edit_distance_batch(lv_ctx* c, size_t npairs, const lv_ct* a, const uint6
                            const lv_ct* b, const uint64_t* b_off, uint32_t symbols,
                            const lv_band* bands, int32_t key_encoding, lv_ct* scores, lv_run* runs) {
   return guard_wf([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     if (symbols < 1)
       throw Error(LV_ERR_INVALID_PARAMS, "equality operands must have the same nonzero symbol count");
     std::vector<PairIn> pairs;
@@ -429,7 +429,7 @@ int lv_eq_table_build(lv_ctx* c, const lv_ct* a, size_t m, uint32_t S, const cha
                       const int32_t* char_symbols, size_t rows, lv_eqtable** out,
                       uint64_t* build_pbs) {
   return guard_wf([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     if (S < 1)
       throw Error(LV_ERR_INVALID_PARAMS, "equality operands must have the same nonzero symbol count");
     check_handles(c, a, m * S);
@@ -497,7 +497,7 @@ int lv_eq_table_lookup(lv_ctx* c, const lv_eqtable* t, char ch, uint64_t positio
 void lv_eq_table_destroy(lv_ctx* c, lv_eqtable* t) {
   if (!t) return;
   if (c) {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     for (auto& kv : t->rows) pool_free(c, kv.second.data(), kv.second.size());
   }
   delete t;
@@ -523,7 +523,7 @@ extern "C" {
 int lv_eq_table_serialize(lv_ctx* c, const lv_eqtable* t, const uint8_t* meta, uint64_t meta_len,
                           uint8_t* buf, uint64_t cap, uint64_t* len) {
   return guard_wf([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     std::vector<uint8_t> b;
     put(b, "LEQT", 4);
     put<uint32_t>(b, 2);
@@ -562,7 +562,7 @@ int lv_eq_table_serialize(lv_ctx* c, const lv_eqtable* t, const uint8_t* meta, u
 int lv_eq_table_deserialize(lv_ctx* c, const uint8_t* buf, uint64_t len, lv_eqtable** out,
                             uint8_t* meta_out, uint64_t meta_cap, uint64_t* meta_len) {
   return guard_wf([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     uint64_t pos = 0;
     auto take = [&](void* dst, uint64_t n) {
       if (pos + n > len) throw Error(LV_ERR_FORMAT, "truncated table file");
@@ -625,7 +625,7 @@ int lv_eq_table_deserialize(lv_ctx* c, const uint8_t* buf, uint64_t len, lv_eqta
 int lv_edit_distance_pre(lv_ctx* c, const lv_eqtable* t, const char* plain, size_t n,
                          const lv_band* band, int32_t key_encoding, lv_ct* score, lv_run* run) {
   return guard_wf([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     PairIn in{(uint32_t)t->length, (uint32_t)n, to_band(band), nullptr, nullptr, t, plain};
     std::vector<PairIn> pairs{in};
     run_traversals(c, pairs, 0, key_encoding == LV_KEY_NEGATED, score, run);
@@ -637,7 +637,7 @@ int lv_edit_distance_pre_batch(lv_ctx* c, size_t npairs, const lv_eqtable* const
                                const lv_band* bands, int32_t key_encoding, lv_ct* scores,
                                lv_run* runs) {
   return guard_wf([&] {
-    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    CtxLock lk(c);
     std::vector<PairIn> pairs;
     pairs.reserve(npairs);
     for (size_t p = 0; p < npairs; ++p) {
