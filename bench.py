@@ -330,7 +330,7 @@ def main():
 
     dist = maybe_init_dist(ws, local)
     torch.cuda.set_device(local)
-    ctx = L.Context(seed=0)
+    ctx = L.Context(seed=0, device=local)
     vals = W.cfg2(BATCH)
     h = ctx.encrypt(vals)
     lid = ctx.lut(L.identity_lut())

@@ -63,6 +63,8 @@ typedef struct {
                                 * the FFT adds no key-amplified noise (phase-noise
                                 * variance within 1.001x of exact integer products;
                                 * 1.4x blind-rotation time). DESIGN.md §2. */
+  int32_t device;              /* CUDA device of the context; -1 (default): the
+                                * calling thread's current device */
 } lv_params;
 
 typedef struct lv_ctx lv_ctx;

@@ -91,7 +91,8 @@ class Params(ctypes.Structure):
                 ("pbs_base_log", ctypes.c_uint32), ("pbs_level", ctypes.c_uint32),
                 ("ks_base_log", ctypes.c_uint32), ("ks_level", ctypes.c_uint32),
                 ("lwe_noise_log2", ctypes.c_uint32), ("glwe_noise_log2", ctypes.c_uint32),
-                ("max_variance_budget", ctypes.c_double), ("exact_mask_product", ctypes.c_uint32)]
+                ("max_variance_budget", ctypes.c_double), ("exact_mask_product", ctypes.c_uint32),
+                ("device", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -270,10 +271,12 @@ class Context:
     """
 
     def __init__(self, seed: int = 0, params: Params | None = None, budget: float | None = None,
-                 _eval_keys=None):
+                 _eval_keys=None, device: int | None = None):
         p = params if params is not None else default_params()
         if budget is not None:
             p.max_variance_budget = float(budget)
+        if device is not None:  # else the calling thread's current CUDA device
+            p.device = int(device)
         self.params = p
         self.seed = seed
         h = ctypes.c_void_p()

@@ -185,8 +185,7 @@ static void launch_keyswitch(lv_ctx* c, const LinDesc* d_desc, uint32_t count, u
 
 // Waves of at most br_pair_max items (default: one per SM) leave SMs idle in
 // the single-CTA form; they run the CTA-pair form instead (2 CTAs per item).
-// Keys with exact_mask_product use the single-CTA exact-mask form at every
-// size.
+// Keys with exact_mask_product use the exact-mask forms of both.
 void launch_blind_rotate(lv_ctx* c, const BrArgs& ba, uint32_t count) {
   if (!count) return;
   if (c->p.exact_mask_product && count <= c->br_pair_max)
@@ -541,6 +540,7 @@ void lv_default_params(lv_params* p) {
   p->glwe_noise_log2 = 17;
   p->max_variance_budget = 4000.0;
   p->exact_mask_product = 0;
+  p->device = -1;
 }
 
 const char* lv_last_error(void) { return g_last_error.c_str(); }
@@ -579,6 +579,8 @@ static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bs
     int ndev = 0;
     LV_CUDA(cudaGetDeviceCount(&ndev));
     if (ndev < 1) throw Error(LV_ERR_CUDA, "no CUDA device");
+    if (p.device >= ndev) throw Error(LV_ERR_INVALID_PARAMS, "device index out of range");
+    if (p.device >= 0) LV_CUDA(cudaSetDevice(p.device));
     lv_ctx* c = new lv_ctx();
     try {
       c->p = p;

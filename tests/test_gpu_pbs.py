@@ -206,3 +206,15 @@ def test_concurrent_host_threads_share_one_context(golden):
         assert c.stats()["pbs_count"] == 6 * 3 * 50
     finally:
         c.close()
+
+
+def test_context_device_selection():
+    """lv_params.device picks the context's GPU (-1: the current device);
+    an index past the device count is InvalidParams."""
+    c = L.Context(seed=2, device=0)
+    try:
+        assert list(c.decrypt(c.pbs(c.encrypt([4]), L.identity_lut()))) == [4]
+    finally:
+        c.close()
+    with pytest.raises(L.InvalidParams):
+        L.Context(seed=2, device=1 << 20)
