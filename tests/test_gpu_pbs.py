@@ -218,3 +218,16 @@ def test_context_device_selection():
         c.close()
     with pytest.raises(L.InvalidParams):
         L.Context(seed=2, device=1 << 20)
+
+
+def test_repeated_batches_bit_identical(ctx):
+    """Race guard (compute-sanitizer is unavailable on the GPU pool): a
+    4096-item batch on the throughput kernel and a 48-item batch on the
+    CTA-pair kernel, each repeated, give bit-identical ciphertexts."""
+    lid = ctx.lut(L.identity_lut())
+    for n in (4096, 48):
+        h = ctx.encrypt([i % 16 for i in range(n)])
+        ref = ctx.export(ctx.pbs(h, lid))
+        for _ in range(2):
+            assert np.array_equal(ref, ctx.export(ctx.pbs(h, lid))), n
+        ctx.release(h)
