@@ -92,6 +92,15 @@ LV_HD int64_t decomp1(uint64_t x, uint32_t base_log) {
   return d;
 }
 
+// decomp1 for the blind-rotation gadget (base 2^23, one level) on 32-bit
+// integer ops: adding 2^40 touches only the high word (2^40 = 2^8 * 2^32),
+// and the arithmetic shift of (hi + 2^8) by 9 is the rounded digit already
+// sign-folded into [-2^22, 2^22) — equal to decomp1(x, 23) for every x.
+static_assert(kPbsBaseLog == 23 && kPbsLevel == 1, "decomp23 is the 2^23 x 1 gadget");
+LV_HD int32_t decomp23(uint64_t x) {
+  return (int32_t)((uint32_t)(x >> 32) + 256u) >> 9;
+}
+
 // Multi-level variant: digits[0] has weight q/B (most significant).
 template <int L>
 LV_HD void decomp(uint64_t x, uint32_t base_log, int64_t* digits) {

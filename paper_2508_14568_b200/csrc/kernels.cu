@@ -162,7 +162,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
           const uint32_t s = (j + 2 * kN - rot) & (2 * kN - 1);
           const uint64_t pv = P[s & (kN - 1)];  // one load; the wrap only flips the sign
           const uint64_t rv = s < kN ? pv : (uint64_t)0 - pv;
-          d[hpart] = (int32_t)decomp1(rv - own[p][2 * r + hpart], kPbsBaseLog);
+          d[hpart] = decomp23(rv - own[p][2 * r + hpart]);
         }
         const double2 tz = TWIST_R(r);
         X[p][r] = cmul(make_double2((double)d[0], (double)d[1]), tz);
@@ -392,7 +392,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
         const uint32_t s = (j + 2 * kN - rot) & (2 * kN - 1);
         const uint64_t pv = acc[s & (kN - 1)];
         const uint64_t rv = s < kN ? pv : (uint64_t)0 - pv;
-        d[hpart] = (int32_t)decomp1(rv - own[2 * r + hpart], kPbsBaseLog);
+        d[hpart] = decomp23(rv - own[2 * r + hpart]);
       }
       X[0][r] = cmul(make_double2((double)d[0], (double)d[1]), tz[r]);
     }
