@@ -21,7 +21,7 @@ ROOT = os.path.dirname(HERE)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-I" + os.path.join(ROOT, "include")]
+         "-I" + os.path.join(ROOT, "include")] + os.environ.get("LVB_NVCC_EXTRA", "").split()
 SOURCES = ["kernels.cu", "ks_tc.cu", "context.cu", "wavefront.cu", "ledger.cpp"]
 
 
