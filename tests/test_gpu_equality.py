@@ -38,3 +38,31 @@ def test_16x16_grid_bootstraps(ctx):
     r = L.compute(a, b, ctx=ctx)
     assert r["pbs_total"] == 768 and r["pbs_equality"] == 512 and r["pbs_kernel"] == 256
     assert r["distance"] == L.wf_distance(a, b) % 32
+
+
+@pytest.mark.parametrize("encoding", ["negated", "original"])
+def test_cell_all_18_inputs(ctx, golden, encoding):
+    """test_kernel.cpp:101-142: the cell over all 18 inputs (dv, dh in
+    {-1, 0, 1}, eq in {0, 1}) in both key encodings, one bootstrap each:
+    key = 3 dh - dv + 9 eq + 4 (negated) or dv + 3 dh + 9 eq + 4 (original,
+    kernel.cpp:152-163), step = PBS(key, min-LUT) = 1 + min(-eq, dv, dh),
+    dv' = step - dh, dh' = step - dv — built here from encrypted operands
+    with the public linear ops."""
+    lut = golden["luts"]["minlut-" + encoding]
+    lid = ctx.lut(lut)
+    combos = [(dv, dh, eq) for dv in (-1, 0, 1) for dh in (-1, 0, 1) for eq in (0, 1)]
+    dv = ctx.encrypt([v % 32 for v, _, _ in combos])
+    dh = ctx.encrypt([h % 32 for _, h, _ in combos])
+    eq9 = ctx.encrypt([9 * e for _, _, e in combos])
+    if encoding == "negated":
+        key = ctx.sub(ctx.scalar_mul(dh, [3] * 18), dv)
+    else:
+        key = ctx.add(dv, ctx.scalar_mul(dh, [3] * 18))
+    key = ctx.scalar_add(ctx.add(key, eq9), [4] * 18)
+    before = ctx.stats()["pbs_count"]
+    step = ctx.pbs(key, lut_ids=[lid] * 18)
+    assert ctx.stats()["pbs_count"] - before == 18  # exactly one bootstrap per cell
+    want = [(1 + min(-e, v, h)) % 32 for v, h, e in combos]
+    assert list(ctx.decrypt(step)) == want
+    assert list(ctx.decrypt(ctx.sub(step, dh))) == [(w - h) % 32 for w, (_, h, _) in zip(want, combos)]
+    assert list(ctx.decrypt(ctx.sub(step, dv))) == [(w - v) % 32 for w, (v, _, _) in zip(want, combos)]
