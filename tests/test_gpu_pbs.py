@@ -231,3 +231,28 @@ def test_repeated_batches_bit_identical(ctx):
         for _ in range(2):
             assert np.array_equal(ref, ctx.export(ctx.pbs(h, lid))), n
         ctx.release(h)
+
+
+@pytest.mark.parametrize("pair_max", [0, 1 << 30])
+def test_other_lwe_dimension_bit_exact(golden, pair_max, monkeypatch):
+    """n is a runtime parameter (only N, k and the gadgets are compiled in):
+    n = 630 keys, key switch and blind rotation stay bit-exact with the
+    oracle at the same parameters, on both blind-rotation kernels."""
+    monkeypatch.setenv("LVB_BR_PAIR_MAX", str(pair_max))
+    from oracle.oracle import Oracle, default_params as oracle_params
+    op = oracle_params()
+    op.n = 630
+    orc = Oracle(seed=3, params=op)
+    p = L.default_params()
+    p.n = 630
+    c = L.Context(seed=3, params=p)
+    try:
+        lut = np.array(golden["luts"]["minlut-negated"], np.int32)
+        lid = c.lut(lut)
+        rows = np.stack([orc.encrypt(v, 4000 + v) for v in (1, 6, 11, 17)])
+        want = orc.pbs_batch(rows, np.tile(lut, (4, 1)))
+        assert np.array_equal(c.pbs_host(rows, [lid] * 4), want)
+        sks, _, ksk, _ = c.debug_keys()
+        assert np.array_equal(sks, orc.sk_small()) and np.array_equal(ksk, orc.ksk())
+    finally:
+        c.close()
