@@ -572,6 +572,9 @@ static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bs
         p.ks_base_log != kKsBaseLog || p.ks_level != kKsLevel)
       throw Error(LV_ERR_INVALID_PARAMS, "parameter set does not match the compiled kernels");
     if (p.n < 1 || p.n > 4096) throw Error(LV_ERR_INVALID_PARAMS, "n out of range");
+    if (p.lwe_noise_log2 < 1 || p.lwe_noise_log2 > 62 || p.glwe_noise_log2 < 1 ||
+        p.glwe_noise_log2 > 62)
+      throw Error(LV_ERR_INVALID_PARAMS, "noise bounds out of range (TUniform 2^1 .. 2^62)");
     if (p.exact_mask_product > 1)
       throw Error(LV_ERR_INVALID_PARAMS, "exact_mask_product must be 0 or 1");
     if (p.max_variance_budget < 1.0)  // backend.hpp:85-88

@@ -47,6 +47,17 @@ def test_evaluation_key_sizes_and_validation(product_lib):
         L.Context.evaluation(np.zeros(7, np.uint64), np.zeros(nk.value, np.uint64), 0)
 
 
+def test_context_rejects_bad_params(product_lib):
+    """Parameter validation happens before any device work (InvalidParams)."""
+    for field, value in (("N", 1024), ("k", 2), ("pbs_base_log", 22), ("ks_level", 4), ("n", 0),
+                         ("n", 5000), ("lwe_noise_log2", 63), ("glwe_noise_log2", 0),
+                         ("exact_mask_product", 2), ("max_variance_budget", 0.5)):
+        p = L.default_params()
+        setattr(p, field, value)
+        with pytest.raises(L.InvalidParams):
+            L.Context(seed=0, params=p)
+
+
 def _band(case):
     m, n = len(case["a"]), len(case["b"])
     mode = case["mode"]
