@@ -189,6 +189,22 @@ def main():
                        "distance": v.value if rc == 0 else None,
                        "error": None if rc == 0 else rc})
     out["banded"] = banded
+    # long single pairs: 300 x 300 printable with 40 substitutions (refreshes
+    # start at the default budget), and a 256 x 256 skip-band DNA pair
+    rng = random.Random(7)
+    a = "".join(chr(32 + rng.randrange(95)) for _ in range(300))
+    bl = list(a)
+    for _ in range(40):
+        i = rng.randrange(len(bl))
+        bl[i] = chr(32 + rng.randrange(95))
+    long_cases = [compute(L, a, "".join(bl))]
+    a = "".join(rng.choice("ACGT") for _ in range(256))
+    bl = list(a)
+    for _ in range(30):
+        i = rng.randrange(len(bl))
+        bl[i] = rng.choice("ACGT")
+    long_cases.append(compute(L, a, "".join(bl), mode="skip", encoding="dna4"))
+    out["long"] = long_cases
     path = os.path.join(HERE, "reference_runs.json")
     with open(path, "w") as f:
         json.dump(out, f, separators=(",", ":"))

@@ -77,3 +77,17 @@ def test_empty_operands():
     assert L.compute("", "abcd")["distance"] == 4
     with pytest.raises(L.BandTooNarrow):
         L.compute("ab", "", mode="skip")
+
+
+def test_long_pairs(golden):
+    """Long single pairs from the compiled reference (golden "long"): a
+    300 x 300 printable pair whose keys reach the default budget (40
+    refreshes; waves grow past the CTA-pair range onto the throughput
+    kernel) and a 256 x 256 skip-band DNA pair. Every RunReport counter and
+    the distance equal the reference's."""
+    for case in golden["long"]:
+        rep = L.compute(case["a"], case["b"], mode=case["mode"], encoding=case["encoding"])
+        want = case["report"]
+        for f in ("distance", "half_width", "visited_cells", "pbs_total", "pbs_equality",
+                  "pbs_kernel", "refresh_count", "max_key_variance", "linear_ops"):
+            assert rep[f] == want[f], (f, rep[f], want[f])
