@@ -38,6 +38,7 @@ constexpr uint32_t kKsBaseLog = 3;
 constexpr uint32_t kKsLevel = 5;
 constexpr uint32_t kLog2N2 = 12;       // log2(2N)
 constexpr uint64_t kDelta = 1ull << 59;
+constexpr uint32_t kMaxLweN = 4096;      // largest small-LWE dimension a context accepts
 
 // Philox domains (shared by specification with the oracle).
 enum Domain : uint32_t {

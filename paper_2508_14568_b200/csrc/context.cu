@@ -571,7 +571,7 @@ static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bs
     if (p.N != kN || p.k != kK || p.pbs_base_log != kPbsBaseLog || p.pbs_level != kPbsLevel ||
         p.ks_base_log != kKsBaseLog || p.ks_level != kKsLevel)
       throw Error(LV_ERR_INVALID_PARAMS, "parameter set does not match the compiled kernels");
-    if (p.n < 1 || p.n > 4096) throw Error(LV_ERR_INVALID_PARAMS, "n out of range");
+    if (p.n < 1 || p.n > kMaxLweN) throw Error(LV_ERR_INVALID_PARAMS, "n out of range");
     if (p.lwe_noise_log2 < 1 || p.lwe_noise_log2 > 62 || p.glwe_noise_log2 < 1 ||
         p.glwe_noise_log2 > 62)
       throw Error(LV_ERR_INVALID_PARAMS, "noise bounds out of range (TUniform 2^1 .. 2^62)");
@@ -592,22 +592,26 @@ static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bs
       LV_CUDA(cudaGetDevice(&c->device));
       LV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       LV_CUDA(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
+      // Function attributes are process-wide, not per context: allow the
+      // dynamic shared memory of the largest supported n, so a context with
+      // a smaller n cannot shrink the limit under another context's launches
+      // (occupancy still follows each launch's actual request).
       LV_CUDA(cudaFuncSetAttribute(blind_rotate_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)blind_rotate_smem_bytes(p.n, false)));
+                                   (int)blind_rotate_smem_bytes(kMaxLweN, false)));
       LV_CUDA(cudaFuncSetAttribute(blind_rotate_exact_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)blind_rotate_smem_bytes(p.n, true)));
+                                   (int)blind_rotate_smem_bytes(kMaxLweN, true)));
       LV_CUDA(cudaFuncSetAttribute(ks_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)ks_tc_smem_bytes()));
       LV_CUDA(cudaFuncSetAttribute(ks_mma_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)ks_tma_smem_bytes()));
       LV_CUDA(cudaFuncSetAttribute(blind_rotate_pair_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)blind_rotate_pair_smem_bytes(p.n)));
+                                   (int)blind_rotate_pair_smem_bytes(kMaxLweN)));
       LV_CUDA(cudaFuncSetAttribute(blind_rotate_pair_exact_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)blind_rotate_pair_smem_bytes(p.n)));
+                                   (int)blind_rotate_pair_smem_bytes(kMaxLweN)));
       {
         int sms = 148;
         LV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
@@ -655,7 +659,7 @@ int lv_ctx_create_eval(const lv_params* params, const uint64_t* bsk, const uint6
 
 int lv_keys_size(const lv_params* params, uint64_t* bsk_count, uint64_t* ksk_count) {
   return guard([&] {
-    if (params->n < 1 || params->n > 4096) throw Error(LV_ERR_INVALID_PARAMS, "n out of range");
+    if (params->n < 1 || params->n > kMaxLweN) throw Error(LV_ERR_INVALID_PARAMS, "n out of range");
     *bsk_count = bsk_words(params->n);
     *ksk_count = ksk_words(params->n);
   });

@@ -256,3 +256,20 @@ def test_other_lwe_dimension_bit_exact(golden, pair_max, monkeypatch):
         assert np.array_equal(sks, orc.sk_small()) and np.array_equal(ksk, orc.ksk())
     finally:
         c.close()
+
+
+def test_contexts_of_different_n_coexist(ctx, orc, golden):
+    """Kernel attributes are process-wide: creating a context with a smaller
+    n must not shrink the shared-memory limit that the default context's
+    launches (larger n) need (regression: 'invalid argument' on the next
+    n = 880 launch after an n = 630 context was created)."""
+    p = L.default_params()
+    p.n = 630
+    small = L.Context(seed=3, params=p)
+    try:
+        lut = np.array(golden["luts"]["minlut-negated"], np.int32)
+        rows = np.stack([orc.encrypt(v, 5000 + v) for v in (2, 9, 20)])
+        want = orc.pbs_batch(rows, np.tile(lut, (3, 1)))
+        assert np.array_equal(ctx.pbs_host(rows, [ctx.lut(lut)] * 3), want)
+    finally:
+        small.close()
