@@ -181,7 +181,11 @@ def traffic_from_profile():
     p = os.path.join(ROOT, "profiles", "latest_br_ncu.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("dram_bytes_per_launch")
+            d = json.load(open(p))
+            if "dram_bytes_per_launch" in d:
+                return d["dram_bytes_per_launch"]
+            br = [x for x in d.get("launches", []) if x.get("kernel") == "blind_rotate_kernel"]
+            return br[0].get("dram_bytes_per_launch") if br else None
         except Exception:
             return None
     return None
