@@ -193,15 +193,15 @@ def traffic_from_profile():
 
 def pipes_from_profile():
     """FP64 / L1 pipe utilisation of the committed ncu capture of the same
-    kernel (profiles/r01_br_full.json): the instruction-level view of the
+    kernel (profiles/latest_br_ncu.json): the instruction-level view of the
     bound beside the algorithmic-FLOP fraction."""
-    p = os.path.join(ROOT, "profiles", "r01_br_full.json")
+    p = os.path.join(ROOT, "profiles", "latest_br_ncu.json")
     try:
         d = json.load(open(p))["launches"][0]
         pct = lambda k: float(d[k].split()[0]) / 100.0  # noqa: E731
         return {"fp64_pipe_active": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
                 "l1tex_throughput": pct("l1tex__throughput.avg.pct_of_peak_sustained_active"),
-                "source": "profiles/r01_br_full.json (ncu --set full)"}
+                "source": "profiles/latest_br_ncu.json (ncu --set full)"}
     except Exception:
         return None
 

@@ -112,11 +112,19 @@ __device__ __forceinline__ double2 mac2(double2 d0, double2 b0, double2 d1, doub
 //
 // Shared memory: acc[2][N] u64 (32 KB) + FFT exchange buffer kXchgBufs x kM
 // double2 (16 KB) + ms[n+1] u16. 168 registers, 3 CTAs/SM.
+// BSK bin groups (of 8) requested inside the forward transform, so their L2
+// latency overlaps its last group. Measured on 4096 items with the
+// evict-last policy: 1 / 2 / 3 / 4 / 5 / 6 / 7 / 8 groups 68.82 / 68.61 /
+// 68.33 / 68.22 / 67.92 / 68.43 / 67.94 / 67.95 ms.
 #ifndef LVB_BSK_EARLY
-#define LVB_BSK_EARLY 2  // BSK bin groups requested inside the forward transform
+#define LVB_BSK_EARLY 5
+#endif
+#ifndef LVB_BSK_EARLY_EXACT
+#define LVB_BSK_EARLY_EXACT 6  // exact-mask kernel (6 values per group): 2 / 3 / 4 / 5 / 6 / 8 groups 93.3 / 92.6 / 89.9 / 90.0 / 89.6 / 89.7 ms
 #endif
 template <bool kExact>
 __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
+  constexpr int kEarly = kExact ? LVB_BSK_EARLY_EXACT : LVB_BSK_EARLY;
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* acc = reinterpret_cast<uint64_t*>(smem);                   // [2][kN]
   double2* buf = reinterpret_cast<double2*>(smem + 2 * kN * 8);        // [kXchgBufs][kM]
@@ -188,17 +196,18 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
 #if LVB_BSK_EARLY
     // the first bins' BSK values are requested before the transform's last
     // group so their L2 latency overlaps it
-    double2 bpre[LVB_BSK_EARLY][kExact ? 6 : 4];
+    static_assert(kEarly >= 1 && kEarly <= 8, "BSK prefetch depth");
+    double2 bpre[kEarly][kExact ? 6 : 4];
     const double2* bsk_row =
         a.bskf + (size_t)i * (8 * (kExact ? 6 : 4) * 128) + t;
     fft_forward<2>(X, buf, tw, t, [&] {
 #pragma unroll
-      for (int q = 0; q < LVB_BSK_EARLY; ++q)
+      for (int q = 0; q < kEarly; ++q)
 #pragma unroll
         for (int e = 0; e < (kExact ? 6 : 4); ++e)
           bpre[q][e] = ld_stream<true>(bsk_row + (q * (kExact ? 6 : 4) + e) * 128);
     });
-#define BSK_AT(q, e, ptr) ((q) < LVB_BSK_EARLY ? bpre[(q) < LVB_BSK_EARLY ? (q) : 0][e] : ld_stream<true>(ptr))
+#define BSK_AT(q, e, ptr) ((q) < kEarly ? bpre[(q) < kEarly ? (q) : 0][e] : ld_stream<true>(ptr))
 #else
     fft_forward<2>(X, buf, tw, t);
 #define BSK_AT(q, e, ptr) ld_stream<true>(ptr)

@@ -5,7 +5,9 @@ import numpy as np
 import paper_2508_14568_b200 as L
 from paper_2508_14568_b200 import workloads as W
 t = time.time()
-c = L.Context(seed=1)
+p = L.default_params()
+p.exact_mask_product = int(os.environ.get("QUICK_EXACT", "0"))  # exact-mask keys
+c = L.Context(seed=1, params=p)
 print("ctx+keygen s", time.time() - t, flush=True)
 vals = W.cfg2()
 h = c.encrypt(vals)
