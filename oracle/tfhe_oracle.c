@@ -230,11 +230,11 @@ static inline void cmul(double ar, double ai, double br, double bi, double* r, d
 }
 
 /* The transform (M = 1024) is a fixed network (the GPU reorders data,
- * never arithmetic): forward = DIF with radix-4 butterflies on the stage pairs
- * (0,1), (3,4), (6,7) and radix-2 stages 2, 5, 8, 9; inverse = DIT with
- * radix-2 stage 9, radix-4 (8,7), radix-2 6, radix-4 (5,4), radix-2 3 and 2,
- * radix-4 (1,0). Output of the forward / input of the inverse: bit-reversed
- * bin order. W^t = exp(-2 pi i t / M) from long double, t < M. */
+ * never arithmetic; csrc/fft.cuh): forward = DIF with radix-4 butterflies on
+ * the stage pairs (0,1), (3,4), (6,7), (8,9) and radix-2 stages 2, 5;
+ * inverse = its DIT mirror: radix-4 (9,8), (7,6), radix-2 5, radix-4 (4,3),
+ * radix-2 2, radix-4 (1,0). Output of the forward / input of the inverse:
+ * bit-reversed bin order. W^t = exp(-2 pi i t / M) from long double, t < M. */
 typedef struct {
   double re, im;
 } cpx;
@@ -293,8 +293,7 @@ static void fft_dif(const orc_ctx* c, double* x /* interleaved M */) {
   r4_dif(c, x, 3);
   r2_dif(c, x, 5);
   r4_dif(c, x, 6);
-  r2_dif(c, x, 8);
-  r2_dif(c, x, 9);
+  r4_dif(c, x, 8); /* k = 0: every twiddle is W^0 */
 }
 
 static void r2_dit(const orc_ctx* c, double* x, uint32_t s) {
@@ -333,11 +332,10 @@ static void fft_dit_inverse(const orc_ctx* c, double* x) {
     for (int s = (int)c->logM - 1; s >= 0; --s) r2_dit(c, x, (uint32_t)s);
     return;
   }
-  r2_dit(c, x, 9);
-  r4_dit(c, x, 7);
-  r2_dit(c, x, 6);
-  r4_dit(c, x, 4);
-  r2_dit(c, x, 3);
+  r4_dit(c, x, 8); /* stages 9, 8 (k = 0) */
+  r4_dit(c, x, 6);
+  r2_dit(c, x, 5);
+  r4_dit(c, x, 3);
   r2_dit(c, x, 2);
   r4_dit(c, x, 0);
 }

@@ -28,6 +28,21 @@ __host__ __device__ constexpr uint32_t r4_base(int s) {
   return s == 0 ? kM : s == 3 ? kM + 768 : s == 4 ? kM + 864 : s == 6 ? kM + 912 : kM + 924;
 }
 constexpr uint32_t kTwEntries = kM + 930;
+// Spectrum layout of the blind rotation (fft.cuh L_D): register n of
+// thread t = 32 w + L holds DIF output position spec_pos(t, n), bits
+// (x0,x1,x6) = n, (x2,x3,x4,x5,x7) = L, (x8,x9) = w. The Fourier BSK is
+// stored in this order; spec_slot is the inverse (t = slot >> 3, n = slot & 7).
+LV_HD uint32_t spec_pos(uint32_t t, uint32_t n) {
+  const uint32_t L = t & 31, w = t >> 5;
+  return (n & 1) | ((n >> 1) & 1) << 1 | ((n >> 2) & 1) << 6 | (L & 1) << 2 | ((L >> 1) & 1) << 3 |
+         ((L >> 2) & 1) << 4 | ((L >> 3) & 1) << 5 | ((L >> 4) & 1) << 7 | (w & 3) << 8;
+}
+LV_HD uint32_t spec_slot(uint32_t x) {
+  const uint32_t n = (x & 1) | ((x >> 1) & 1) << 1 | ((x >> 6) & 1) << 2;
+  const uint32_t L = ((x >> 2) & 1) | ((x >> 3) & 1) << 1 | ((x >> 4) & 1) << 2 | ((x >> 5) & 1) << 3 |
+                     ((x >> 7) & 1) << 4;
+  return ((((x >> 8) & 3) * 32 + L) << 3) | n;
+}
 constexpr uint32_t kK = 1;             // GLWE dimension
 constexpr uint32_t kBig = kK * kN;     // big-key LWE mask length
 constexpr uint32_t kBigStride = kBig + 8;  // pool row stride in u64 (16448 B, 64 B aligned)

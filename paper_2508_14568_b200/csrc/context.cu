@@ -1002,14 +1002,14 @@ int lv_debug_keys(lv_ctx* c, uint8_t* sk_small, uint8_t* sk_glwe, uint64_t* ksk,
     if (bskf_nat) {
       std::vector<double2> raw((size_t)n * 32 * 128);
       LV_CUDA(cudaMemcpy(raw.data(), c->d_bskf, raw.size() * sizeof(double2), cudaMemcpyDeviceToHost));
-      // device [i][q*4 + r*2 + o][t] -> oracle [(i*rows + r)*(k+1) + o][f = 8t+q] (re, im)
+      // device [i][q*4 + r*2 + o][t] -> oracle [(i*rows + r)*(k+1) + o][f = spec_pos(t, q)] (re, im)
       for (size_t i = 0; i < n; ++i)
         for (uint32_t q = 0; q < 8; ++q)
           for (uint32_t r = 0; r < 2; ++r)
             for (uint32_t o = 0; o < 2; ++o)
               for (uint32_t t = 0; t < 128; ++t) {
                 const double2 v = raw[i * 4096 + (q * 4 + r * 2 + o) * 128 + t];
-                const size_t base = ((i * kRows + r) * (kK + 1) + o) * 2 * kM + 2 * (8 * t + q);
+                const size_t base = ((i * kRows + r) * (kK + 1) + o) * 2 * kM + 2 * spec_pos(t, q);
                 bskf_nat[base] = v.x * 1024.0;  // undo the exact 2^-10 pre-scaling
                 bskf_nat[base + 1] = v.y * 1024.0;
               }

@@ -5,31 +5,40 @@
 // Bit-exactness contract with oracle/tfhe_oracle.c (fft_dif,
 // fft_dit_inverse, forward_i64, backward_torus): the network is fixed —
 // forward: radix-4 DIF butterflies on the stage pairs (0,1), (3,4), (6,7),
-// radix-2 stages 2, 5, 8, 9; inverse: radix-2 DIT stage 9, radix-4 (8,7),
-// radix-2 6, radix-4 (5,4), radix-2 3 and 2, radix-4 (1,0) — and every
+// (8,9) and radix-2 stages 2, 5; inverse (its DIT mirror): radix-4 (9,8),
+// (7,6), radix-2 5, radix-4 (4,3), radix-2 2, radix-4 (1,0) — and every
 // butterfly performs exactly the oracle's IEEE operations (__dadd_rn /
 // __dsub_rn for sums, cmul() = {fma(a.x,b.x,-(a.y*b.y)), fma(a.x,b.y,(a.y*b.x))}
 // for twiddles, the same table entries). Only the data movement differs
-// (registers, a swizzled shared buffer, lane shuffles), which cannot change
+// (registers, a swizzled shared buffer, tensor memory), which cannot change
 // a rounding. Multiplications by W^0 = (1,-0) that are static are skipped:
-// they are exact up to the sign of zero, which never reaches a nonzero result.
-// The radix-4 pairing saves a quarter of those stages' twiddle products
-// (-8% FP64 instructions per transform) and rounds no more often
-// (tools/fft_error.c: external-product error std 2^37.96 vs 2^38.00).
+// they are exact up to the sign of zero, which never reaches a nonzero
+// result (the (8,9) pair's twiddles are all W^0).
 //
-// Thread layouts (t = threadIdx.x in [0,128), r = register index 0..7):
-//   fwd A  (stages 0-2) : x = t + 128 r
-//   fwd B  (stages 3-5) : t = 16 b + u,   x = 128 b + u + 16 r
-//   fwd C  (stages 6-8) : t = 2 c + v,    x = 16 c + v + 2 r
-//   fwd stage 9 via shfl.xor 1 -> thread t owns spectrum bins 8t .. 8t+7
-//   inv    (stages 9-7) : bins 8t + r
-//   inv B' (stages 6-4) : t = 8 b + u,    x = 64 b + u + 8 r
-//   inv stage 3 via shfl.xor 8
-//   inv A  (stages 2-0) : x = t + 128 r
-// In every group the radix-4 quadruples are the registers (r, r+2, r+4,
-// r+6), r in {0, 1}, and the radix-2 pairs (r, r+1), r even.
-// Shared buffer index swizzle swz(x) keeps every one of these patterns
-// free of bank conflicts (16-byte elements, 8 lanes per 128-byte wavefront).
+// Data movement per transform: one cross-warp exchange through shared
+// memory and two warp-local exchanges through TENSOR MEMORY. A TMEM round
+// trip — tcgen05.st with the 32x32b shape (thread = lane, registers =
+// columns), tcgen05.ld with the 16x256b shape (thread t0 + 4 t1 <- lane
+// t1 + 8h (+16 for the second load), 64-bit column t0 + 4k) — permutes the
+// data between the warp's threads: it moves lane bits 3,4 into registers
+// and register bits 0,1 into lanes. TMEM traffic runs on its own datapath,
+// not the L1/shared-memory pipe that bounds this kernel (tools/
+// tmem_xchg_bench.cu: a round trip of 2 x 4 KB per warp costs 271 SM-cycles
+// per CTA vs 539 for the shared-memory exchange it replaces, and mixed
+// with shared-memory traffic the two overlap completely). Complex points
+// are stored planar (re of point r at 64-bit column r, im at 8 + r) so a
+// 16x256b fragment keeps each point's two halves in one thread.
+//
+// Thread layouts (t = 32 w + L, w = warp, L = lane, r / n = register 0..7;
+// x = position, bits x9..x0):
+//   L_A (fwd pass A / inv pass A'): x = t + 128 r: regs (x7,x8,x9),
+//        lanes (x0..x4), warps (x5,x6)
+//   L_B : regs (x4,x5,x6), lanes (x7,x0,x1,x2,x3), warps (x8,x9)
+//   L_C : regs (x2,x3,x6), lanes (x4,x5,x7,x0,x1)
+//   L_D : regs (x0,x1,x6), lanes (x2,x3,x4,x5,x7)  — the spectrum layout
+// L_A <-> L_B cross warps (shared memory); L_B -> L_C -> L_D are TMEM
+// round trips (32x32b store, 16x256b load) and the inverse walks back with
+// the inverse trips (16x256b store, 32x32b load).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -38,64 +47,270 @@
 
 namespace lvb {
 
-__device__ __forceinline__ uint32_t swz(uint32_t x) {
-  return x ^ ((((x >> 3) & 7u) ^ (((x >> 9) & 1u) << 2)));
-}
+// Shared buffer index swizzle: both L_A (x0..x2 across an 8-lane phase,
+// x7 fixed) and L_B (x7, x0, x1 across a phase, x2 fixed) hit 8 distinct
+// 16-byte bank groups.
+__device__ __forceinline__ uint32_t swz(uint32_t x) { return x ^ (((x >> 7) & 1u) << 2); }
 
-// Exchange through shared memory: one polynomial at a time through a
-// single kM-entry buffer (16 KB) instead of all P at once (smaller shared
-// footprint). Set LVB_SPLIT_XCHG=0 for the P-buffer form.
-#ifndef LVB_SPLIT_XCHG
-#define LVB_SPLIT_XCHG 1
-#endif
-constexpr bool kSplitXchg = LVB_SPLIT_XCHG;
-constexpr int kXchgBufs = kSplitXchg ? 1 : 2;
-#ifndef LVB_TW_EARLY
-#define LVB_TW_EARLY 1  // twiddles requested before the exchange that precedes their group
-#endif
+// Barrier of the threads sharing one transform (the CTA).
+struct CtaBar {
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
 
-// Moves X from layout wr(r) to layout rd(r) (element indices x).
-// kWarp: both layouts keep warp w inside the 256-point block w (x >> 8 = w;
-// swz() preserves it), so only this warp reads or writes that part of the
-// buffer and __syncwarp orders the exchange. Otherwise the exchange crosses
-// warps: the caller guarantees no other warp still reads the addresses
-// written (this warp's own earlier reads are ordered here).
-template <int P, bool kWarp = false, typename WR, typename RD>
-__device__ __forceinline__ void xchg(double2 (&X)[P][8], double2* buf, WR wr, RD rd) {
+// Cross-warp exchanges go through NB shared 16 KB buffers (P polynomials in
+// groups of NB). LVB_XCHG_BUFS=1 trades two barriers per exchange for 16 KB.
+#ifndef LVB_XCHG_BUFS
+#define LVB_XCHG_BUFS 2
+#endif
+constexpr int kXchgBufs = LVB_XCHG_BUFS;
+
+// Moves X from layout wr(r) to layout rd(r) (element indices x) across
+// warps. The caller guarantees no warp still reads the buffer.
+template <int P, int NB, typename Bar, typename WR, typename RD>
+__device__ __forceinline__ void xchg_cta(double2 (&X)[P][8], double2* buf, const Bar& bar, WR wr,
+                                         RD rd) {
 #ifdef LVB_ABL_XCHG  // timing ablation only: results are wrong
-  __syncthreads();
+  bar.sync();
   return;
 #endif
-  auto sync = [] {
-    if constexpr (kWarp)
-      __syncwarp();
-    else
-      __syncthreads();
-  };
-  __syncwarp();
-  if constexpr (!kSplitXchg || P == 1) {
 #pragma unroll
-    for (int p = 0; p < P; ++p)
+  for (int p0 = 0; p0 < P; p0 += NB) {
+    if (p0) bar.sync();
 #pragma unroll
-      for (int r = 0; r < 8; ++r) buf[p * kM + swz(wr(r))] = X[p][r];
-    sync();
+    for (int p = p0; p < P && p < p0 + NB; ++p)
 #pragma unroll
-    for (int p = 0; p < P; ++p)
+      for (int r = 0; r < 8; ++r) buf[(p - p0) * kM + swz(wr(r))] = X[p][r];
+    bar.sync();
 #pragma unroll
-      for (int r = 0; r < 8; ++r) X[p][r] = buf[p * kM + swz(rd(r))];
-  } else {
+    for (int p = p0; p < P && p < p0 + NB; ++p)
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      if (p) sync();
-#pragma unroll
-      for (int r = 0; r < 8; ++r) buf[swz(wr(r))] = X[p][r];
-      sync();
-#pragma unroll
-      for (int r = 0; r < 8; ++r) X[p][r] = buf[swz(rd(r))];
-    }
+      for (int r = 0; r < 8; ++r) X[p][r] = buf[(p - p0) * kM + swz(rd(r))];
   }
 }
 
+// ---------------------------------------------------------------- TMEM
+// Allocation: warp 0 allocates ncols columns (power of 2, >= 32) and
+// writes the base address to *slot; every thread returns it.
+__device__ __forceinline__ uint32_t tmem_alloc(uint32_t* slot, uint32_t ncols) {
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(slot)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  return *slot;
+}
+__device__ __forceinline__ void tmem_free(uint32_t base, uint32_t ncols) {
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (threadIdx.x < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(ncols));
+}
+// This warp's lane quarter of the CTA's allocation.
+__device__ __forceinline__ uint32_t tmem_warp_base(uint32_t base) {
+  return base + ((32u * ((threadIdx.x >> 5) & 3u)) << 16);
+}
+constexpr uint32_t kTmemColsPerPoly = 32;  // 8 complex points x 4 columns
+
+__device__ __forceinline__ uint32_t d_lo(double v) { return (uint32_t)__double_as_longlong(v); }
+__device__ __forceinline__ uint32_t d_hi(double v) {
+  return (uint32_t)((unsigned long long)__double_as_longlong(v) >> 32);
+}
+__device__ __forceinline__ double d_mk(uint32_t l, uint32_t h) {
+  return __longlong_as_double((long long)(((unsigned long long)h << 32) | l));
+}
+
+// tcgen05.wait::ld that also names the loaded registers as in/out
+// operands, so the compiler cannot schedule a use of them above the wait.
+#define LVB_TM_WAIT_LD16(a, b)                                                                    \
+  asm volatile("tcgen05.wait::ld.sync.aligned;"                                                   \
+               : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]),          \
+                 "+r"(a[6]), "+r"(a[7]), "+r"(a[8]), "+r"(a[9]), "+r"(a[10]), "+r"(a[11]),        \
+                 "+r"(a[12]), "+r"(a[13]), "+r"(a[14]), "+r"(a[15]), "+r"(b[0]), "+r"(b[1]),      \
+                 "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7]),          \
+                 "+r"(b[8]), "+r"(b[9]), "+r"(b[10]), "+r"(b[11]), "+r"(b[12]), "+r"(b[13]),      \
+                 "+r"(b[14]), "+r"(b[15])                                                         \
+               :                                                                                  \
+               : "memory")
+
+// LVB_TM_FINE: one tcgen05 instruction per double (32x32b.x2) / per two
+// doubles (16x256b.x1) instead of one per 8 points, so the operands need
+// only aligned register pairs, not 16- or 32-register blocks (no moves).
+#ifndef LVB_TM_FINE
+#define LVB_TM_FINE 0
+#endif
+__device__ __forceinline__ void tm_st_32x32b(uint32_t a, const double2 (&X)[8]) {
+#if LVB_TM_FINE
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(a + 2 * k),
+                 "r"(d_lo(X[k].x)), "r"(d_hi(X[k].x))
+                 : "memory");
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(a + 16 + 2 * k),
+                 "r"(d_lo(X[k].y)), "r"(d_hi(X[k].y))
+                 : "memory");
+  }
+  return;
+#endif
+  uint32_t r[32];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    r[2 * k] = d_lo(X[k].x);
+    r[2 * k + 1] = d_hi(X[k].x);
+    r[16 + 2 * k] = d_lo(X[k].y);
+    r[17 + 2 * k] = d_hi(X[k].y);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(a),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]),
+      "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]),
+      "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+// Issues the load; the caller waits (LVB_TM_WAIT_LD16(r, r + 16)) and unpacks.
+__device__ __forceinline__ void tm_ld_32x32b(uint32_t a, uint32_t (&r)[32]) {
+#if LVB_TM_FINE
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                 : "=r"(r[2 * k]), "=r"(r[2 * k + 1])
+                 : "r"(a + 2 * k)
+                 : "memory");
+  return;
+#endif
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(a)
+      : "memory");
+}
+__device__ __forceinline__ void unpack32(const uint32_t (&r)[32], double2 (&X)[8]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    X[k] = make_double2(d_mk(r[2 * k], r[2 * k + 1]), d_mk(r[16 + 2 * k], r[17 + 2 * k]));
+}
+// 16x256b fragment of 16 lanes (the lane base is in the address) x 32
+// columns: reg 4k + 2h (+1) = lane t1 + 8h, 64-bit column 4k + t0.
+#if LVB_TM_FINE
+#define LVB_TM_16x256b_LD(addr, a)                                                               \
+  do {                                                                                           \
+    _Pragma("unroll") for (int k_ = 0; k_ < 4; ++k_) asm volatile(                              \
+        "tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"                            \
+        : "=r"(a[4 * k_]), "=r"(a[4 * k_ + 1]), "=r"(a[4 * k_ + 2]), "=r"(a[4 * k_ + 3])         \
+        : "r"((addr) + 8 * k_)                                                                   \
+        : "memory");                                                                             \
+  } while (0)
+#define LVB_TM_16x256b_ST(addr, a)                                                               \
+  do {                                                                                           \
+    _Pragma("unroll") for (int k_ = 0; k_ < 4; ++k_) asm volatile(                              \
+        "tcgen05.st.sync.aligned.16x256b.x1.b32 [%0], {%1,%2,%3,%4};" ::"r"((addr) + 8 * k_),    \
+        "r"(a[4 * k_]), "r"(a[4 * k_ + 1]), "r"(a[4 * k_ + 2]), "r"(a[4 * k_ + 3])              \
+        : "memory");                                                                             \
+  } while (0)
+#else
+#define LVB_TM_16x256b_LD(addr, a)                                                                \
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12," \
+               "%13,%14,%15}, [%16];"                                                              \
+               : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]),           \
+                 "=r"(a[6]), "=r"(a[7]), "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]),         \
+                 "=r"(a[12]), "=r"(a[13]), "=r"(a[14]), "=r"(a[15])                                \
+               : "r"(addr)                                                                         \
+               : "memory")
+#define LVB_TM_16x256b_ST(addr, a)                                                                 \
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11," \
+               "%12,%13,%14,%15,%16};" ::"r"(addr),                                                \
+               "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]),        \
+               "r"(a[7]), "r"(a[8]), "r"(a[9]), "r"(a[10]), "r"(a[11]), "r"(a[12]), "r"(a[13]),    \
+               "r"(a[14]), "r"(a[15])                                                              \
+               : "memory")
+#endif
+// Point index n of the 16x256b view: n = h + 2 g + 4 k' <-> (lane t1 + 8h +
+// 16g, stored point t0 + 4k'); re at columns 4k', im at 4(k' + 2).
+template <int G>
+__device__ __forceinline__ void unpack16(const uint32_t (&a)[16], double2 (&X)[8]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      X[h + 2 * G + 4 * k] = make_double2(d_mk(a[4 * k + 2 * h], a[4 * k + 2 * h + 1]),
+                                          d_mk(a[4 * (k + 2) + 2 * h], a[4 * (k + 2) + 2 * h + 1]));
+}
+template <int G>
+__device__ __forceinline__ void pack16(const double2 (&X)[8], uint32_t (&a)[16]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double2 v = X[h + 2 * G + 4 * k];
+      a[4 * k + 2 * h] = d_lo(v.x);
+      a[4 * k + 2 * h + 1] = d_hi(v.x);
+      a[4 * (k + 2) + 2 * h] = d_lo(v.y);
+      a[4 * (k + 2) + 2 * h + 1] = d_hi(v.y);
+    }
+}
+
+// Forward trip: lanes (l0..l4), regs (r0,r1,r2) -> lanes (r0,r1,l0,l1,l2),
+// regs (l3,l4,r2). tm = this warp's lane-quarter base; polynomial p uses
+// columns [32p, 32p + 32).
+template <int P>
+__device__ __forceinline__ void tm_trip_fwd(double2 (&X)[P][8], uint32_t tm) {
+#ifdef LVB_ABL_TMEM  // timing ablation only
+  return;
+#endif
+#pragma unroll
+  for (int p = 0; p < P; ++p) tm_st_32x32b(tm + p * kTmemColsPerPoly, X[p]);
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  uint32_t a[P][16], b[P][16];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    LVB_TM_16x256b_LD(tm + p * kTmemColsPerPoly, a[p]);
+    LVB_TM_16x256b_LD(tm + p * kTmemColsPerPoly + (16u << 16), b[p]);
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    LVB_TM_WAIT_LD16(a[p], b[p]);  // the first wait covers every load; the rest fence registers
+    unpack16<0>(a[p], X[p]);
+    unpack16<1>(b[p], X[p]);
+  }
+}
+// Inverse trip (undoes tm_trip_fwd): lanes (l0..l4), regs (r0,r1,r2) ->
+// lanes (l2,l3,l4,r0,r1), regs (l0,l1,r2).
+template <int P>
+__device__ __forceinline__ void tm_trip_inv(double2 (&X)[P][8], uint32_t tm) {
+#ifdef LVB_ABL_TMEM
+  return;
+#endif
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    uint32_t a[16], b[16];
+    pack16<0>(X[p], a);
+    pack16<1>(X[p], b);
+    LVB_TM_16x256b_ST(tm + p * kTmemColsPerPoly, a);
+    LVB_TM_16x256b_ST(tm + p * kTmemColsPerPoly + (16u << 16), b);
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  uint32_t r[P][32];
+#pragma unroll
+  for (int p = 0; p < P; ++p) tm_ld_32x32b(tm + p * kTmemColsPerPoly, r[p]);
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    LVB_TM_WAIT_LD16(r[p], (r[p] + 16));
+    unpack32(r[p], X[p]);
+  }
+}
+
+// ---------------------------------------------------------------- math
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   const double t1 = __dmul_rn(a.y, b.y);
   const double t2 = __dmul_rn(a.y, b.x);
@@ -123,19 +338,9 @@ __device__ __forceinline__ void dif(double2& u, double2& v, double2 w) {
   u = s;
   v = cmul(d, w);
 }
-__device__ __forceinline__ void dif1(double2& u, double2& v) {  // w = W^0
-  const double2 s = add2(u, v), d = sub2(u, v);
-  u = s;
-  v = d;
-}
 __device__ __forceinline__ void dit(double2& p, double2& q, double2 w) {
   const double2 qw = cmul_conj(q, w);
   const double2 a = add2(p, qw), b = sub2(p, qw);
-  p = a;
-  q = b;
-}
-__device__ __forceinline__ void dit1(double2& p, double2& q) {  // w = W^0
-  const double2 a = add2(p, q), b = sub2(p, q);
   p = a;
   q = b;
 }
@@ -150,6 +355,14 @@ __device__ __forceinline__ void dif4(double2& x0, double2& x1, double2& x2, doub
   x1 = cmul(sub2(A, B), w2);
   x2 = cmul(add2(C, D), w1);
   x3 = cmul(sub2(C, D), w3);
+}
+__device__ __forceinline__ void dif4_1(double2& x0, double2& x1, double2& x2, double2& x3) {  // k = 0
+  const double2 A = add2(x0, x2), B = add2(x1, x3), C = sub2(x0, x2), d = sub2(x1, x3);
+  const double2 D = make_double2(d.y, -d.x);
+  x0 = add2(A, B);
+  x1 = sub2(A, B);
+  x2 = add2(C, D);
+  x3 = sub2(C, D);
 }
 // radix-4 DIT on stages s+1 then s (oracle r4_dit).
 __device__ __forceinline__ void dit4(double2& x0, double2& x1, double2& x2, double2& x3,
@@ -174,8 +387,8 @@ __device__ __forceinline__ void dit4_1(double2& x0, double2& x1, double2& x2, do
 // Twiddle tables (one buffer, built by context.cu build_tables):
 //   [0, kM): per-stage radix-2 tables T_s[y] = W[y << s] (W[k] =
 //            exp(-2 pi i k / kM)) concatenated, T_s at kM - (kM >> s);
-//   then per radix-4 pair s in {0, 3, 4, 6, 7}: three planes of H = kM >> (s+2)
-//            entries, plane m (1..3) holding W[m (j << s)].
+//   then per radix-4 pair s: three planes of H = kM >> (s+2) entries,
+//            plane m (1..3) holding W[m (j << s)].
 // Same values as the oracle's W table, laid out so every warp-wide load is
 // contiguous or a broadcast.
 __device__ __forceinline__ double2 tws(const double2* __restrict__ tw, int s, uint32_t y) {
@@ -185,6 +398,9 @@ __device__ __forceinline__ double2 tws(const double2* __restrict__ tw, int s, ui
   return __ldg(tw + (kM - (kM >> s)) + y);
 }
 __device__ __forceinline__ double2 tw4(const double2* __restrict__ tw, int s, int m, uint32_t j) {
+#ifdef LVB_ABL_TW
+  return make_double2(0.70710678118654757 + s * 1e-3, 0.70710678118654757 - j * 1e-9 - m);
+#endif
   return __ldg(tw + r4_base(s) + (m - 1) * (kM >> (s + 2)) + j);
 }
 
@@ -198,239 +414,146 @@ __device__ __forceinline__ double2 twist_at(const double2* __restrict__ fine, ui
   return (x >> 7) == 0 ? f : cmul(f, c_twist_coarse[x >> 7]);
 }
 
-__device__ __forceinline__ double2 shfl_xor_d2(double2 v, int m) {
-  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
-}
-
 // ---------------------------------------------------------------- forward
-// X[p][r] on entry: twisted inputs at x = t + 128 r. On exit: spectrum
-// bins 8t + r. buf: the exchange buffer(s).
+// X[p][r] on entry: twisted inputs at x = t + 128 r (L_A). On exit: the
+// spectrum in L_D (register n of thread t = position spec_pos(t, n)).
+// buf: NB exchange buffers (no warp may still be reading them); tm: this
+// warp's TMEM lane-quarter base.
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
-// hook() runs once group C's data has arrived (the caller issues loads it
-// needs right after the transform there, e.g. the first BSK row).
-template <int P, typename Hook = NoHook>
+// hook() runs after the first TMEM trip (the caller issues loads it needs
+// right after the transform there, e.g. the first BSK row).
+template <int P, int NB = kXchgBufs, typename Hook = NoHook, typename Bar = CtaBar>
 __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
-                                            const double2* __restrict__ tw, uint32_t t,
-                                            Hook hook = Hook()) {
-  // group A: radix-4 (0,1) with k = t + 128 r, radix-2 stage 2
+                                            const double2* __restrict__ tw, uint32_t t, uint32_t tm,
+                                            Hook hook = Hook(), Bar bar = Bar()) {
+  const uint32_t L = t & 31, w = t >> 5;
+  // pass A (L_A): radix-4 (0,1) with j = t + 128 r, radix-2 stage 2 (j = t)
   {
-    double2 w[2][3];
+    double2 w4[2][3];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
-      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 0, m + 1, t + 128 * r);
+      for (int m = 0; m < 3; ++m) w4[r][m] = tw4(tw, 0, m + 1, t + 128 * r);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 2; ++r)
-        dif4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w[r][0], w[r][1], w[r][2]);
+        dif4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w4[r][0], w4[r][1], w4[r][2]);
     const double2 w2 = tws(tw, 2, t);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; r += 2) dif(X[p][r], X[p][r + 1], w2);
   }
-  // A -> B: radix-4 (3,4) with j = u + 16 r, radix-2 stage 5
+  // L_A -> L_B (cross-warp); pass B: radix-4 (3,4) on (x5, x6) = regs
+  // (r1, r2), j = x mod 32 = 16 x4 + u; radix-2 stage 5 on x4 = r0, j = u
+  const uint32_t u = L >> 1;  // x3..x0
   {
-    const uint32_t b = t >> 4, u = t & 15;
-#if LVB_TW_EARLY
-    double2 w[2][3];
+    double2 w4[2][3];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
-      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 3, m + 1, u + 16 * r);
-    xchg<P>(X, buf, [&](int r) { return t + 128 * r; },
-            [&](int r) { return 128 * b + u + 16 * r; });
-#else
-    xchg<P>(X, buf, [&](int r) { return t + 128 * r; },
-            [&](int r) { return 128 * b + u + 16 * r; });
-    double2 w[2][3];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 3, m + 1, u + 16 * r);
-#endif
+      for (int m = 0; m < 3; ++m) w4[r][m] = tw4(tw, 3, m + 1, u + 16 * r);
+    xchg_cta<P, NB>(X, buf, bar, [&](int r) { return t + 128u * r; },
+                    [&](int r) { return 16u * r + 128u * (L & 1) + u + 256u * w; });
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 2; ++r)
-        dif4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w[r][0], w[r][1], w[r][2]);
+        dif4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w4[r][0], w4[r][1], w4[r][2]);
     const double2 w5 = tws(tw, 5, u);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 8; r += 2) dif(X[p][r], X[p][r + 1], w5);
-#if LVB_TW_EARLY
-    const uint32_t v0 = t & 1;
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 6, m + 1, v0 + 2 * r);
-#endif
-    // B and C both keep warp w in block w (x >> 8 = t >> 5): warp-local
-    const uint32_t c = t >> 1, v = t & 1;
-    xchg<P, true>(X, buf, [&](int r) { return 128 * b + u + 16 * r; },
-                  [&](int r) { return 16 * c + v + 2 * r; });
-    hook();
-#if LVB_TW_EARLY
-    // group C continues in this scope (w already holds its twiddles)
-#else
   }
-  // C: radix-4 (6,7) with j = v + 2 r, radix-2 stage 8, stage 9 by shuffle
+  // L_B -> L_C (TMEM); pass C: radix-4 (6,7) on (x2, x3) = regs (n0, n1),
+  // j = x mod 4 = (x0, x1) = lanes (3, 4)
   {
-    const uint32_t v = t & 1;
-    double2 w[2][3];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 6, m + 1, v + 2 * r);
-#endif
+    const uint32_t j = L >> 3;
+    const double2 w1 = tw4(tw, 6, 1, j), w2 = tw4(tw, 6, 2, j), w3 = tw4(tw, 6, 3, j);
+    tm_trip_fwd<P>(X, tm);
+    hook();
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
-        dif4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w[r][0], w[r][1], w[r][2]);
-    const double2 w8 = tws(tw, 8, v);
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int r = 0; r < 8; r += 2) dif(X[p][r], X[p][r + 1], w8);
-    // stage 9: pairs (16c + 2r, 16c + 2r + 1) live in lanes (2c, 2c+1).
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      double2 Y[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) Y[q] = shfl_xor_d2(v ? X[p][q] : X[p][4 + q], 1);
-      double2 F[8];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        double2 e = v ? Y[q] : X[p][q];
-        double2 o = v ? X[p][4 + q] : Y[q];
-        dif1(e, o);
-        F[2 * q] = e;
-        F[2 * q + 1] = o;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) X[p][q] = F[q];
-    }
+      for (int n = 0; n < 8; n += 4) dif4(X[p][n], X[p][n + 1], X[p][n + 2], X[p][n + 3], w1, w2, w3);
   }
+  // L_C -> L_D (TMEM); pass D: radix-4 (8,9) on (x0, x1) = regs (n0, n1), k = 0
+  tm_trip_fwd<P>(X, tm);
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+#pragma unroll
+    for (int n = 0; n < 8; n += 4) dif4_1(X[p][n], X[p][n + 1], X[p][n + 2], X[p][n + 3]);
 }
 
 // ------------------------------------------------------------- inverse
-// X[p][r] on entry: spectrum bins 8t + r. On exit: layout A (x = t + 128 r),
-// the layout fft_forward's input uses, so each thread owns the same
-// accumulator coefficients in both halves of a CMUX. The first exchange is
-// warp-local, so the caller only has to order this warp's earlier buffer
-// reads (__syncwarp).
-template <int P>
+// X[p][r] on entry: the spectrum in L_D. On exit: L_A (x = t + 128 r), the
+// layout fft_forward's input uses, so each thread owns the same
+// accumulator coefficients in both halves of a CMUX. The cross-warp
+// exchange starts with a CTA barrier (other warps may still read buf).
+template <int P, int NB = kXchgBufs, typename Bar = CtaBar>
 __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
-                                              const double2* __restrict__ tw, uint32_t t) {
-  // stage 9 (W^0), radix-4 (8,7): j = r, k = 128 r (r = 0: W^0)
+                                              const double2* __restrict__ tw, uint32_t t,
+                                              uint32_t tm, Bar bar = Bar()) {
+  const uint32_t L = t & 31, w = t >> 5;
+  // pass D': radix-4 (9,8) on (x0, x1) = regs (n0, n1), k = 0
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+#pragma unroll
+    for (int n = 0; n < 8; n += 4) dit4_1(X[p][n], X[p][n + 1], X[p][n + 2], X[p][n + 3]);
+  // L_D -> L_C (TMEM); pass C': radix-4 (7,6) on (x2, x3), j = lanes (3, 4)
   {
-    const double2 w1 = tw4(tw, 7, 1, 1), w2 = tw4(tw, 7, 2, 1), w3 = tw4(tw, 7, 3, 1);
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-#pragma unroll
-      for (int r = 0; r < 8; r += 2) dit1(X[p][r], X[p][r + 1]);
-      dit4_1(X[p][0], X[p][2], X[p][4], X[p][6]);
-      dit4(X[p][1], X[p][3], X[p][5], X[p][7], w1, w2, w3);
-    }
-  }
-  const uint32_t b = t >> 3, u = t & 7, odd = b & 1;
-#if LVB_TW_EARLY
-  const double2 w6 = tws(tw, 6, u);
-  double2 w[2][3];
-#pragma unroll
-  for (int r = 0; r < 2; ++r)
-#pragma unroll
-    for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 4, m + 1, u + 8 * r);
-#endif
-  // bins 8t + r and B' both keep warp w in block w: warp-local
-  xchg<P, true>(X, buf, [&](int r) { return 8 * t + r; },
-                [&](int r) { return 64 * b + u + 8 * r; });
-  {
-    // stage 6, radix-4 (5,4) with j = u + 8 r
-#if !LVB_TW_EARLY
-    const double2 w6 = tws(tw, 6, u);
-#endif
+    const uint32_t j = L >> 3;
+    const double2 w1 = tw4(tw, 6, 1, j), w2 = tw4(tw, 6, 2, j), w3 = tw4(tw, 6, 3, j);
+    tm_trip_inv<P>(X, tm);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w6);
-#if !LVB_TW_EARLY
-    double2 w[2][3];
+      for (int n = 0; n < 8; n += 4) dit4(X[p][n], X[p][n + 1], X[p][n + 2], X[p][n + 3], w1, w2, w3);
+  }
+  // L_C -> L_B (TMEM); pass B': radix-2 stage 5 on x4 = r0 (j = u), then
+  // radix-4 (4,3) on (x5, x6) = (r1, r2), j = u + 16 x4
+  const uint32_t u = L >> 1;
+  double2 w4[2][3];
+  {
+    const double2 w5 = tws(tw, 5, u);
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
-      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 4, m + 1, u + 8 * r);
-#endif
+      for (int m = 0; m < 3; ++m) w4[r][m] = tw4(tw, 3, m + 1, u + 16 * r);
+    tm_trip_inv<P>(X, tm);
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w5);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
       for (int r = 0; r < 2; ++r)
-        dit4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w[r][0], w[r][1], w[r][2]);
-    // stage 3 (half 64): even b holds x, odd b holds x + 64; even lane
-    // finishes r = 0..3, odd lane r = 4..7
-    double2 w3[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) w3[q] = tws(tw, 3, u + 8 * (q + 4 * odd));
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      double2 Y[4];
-      // even lane needs the odd lane's X[q] (upper of r=q); odd lane needs
-      // the even lane's X[4+q] (lower of r=4+q)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) Y[q] = shfl_xor_d2(odd ? X[p][q] : X[p][4 + q], 8);
-      double2 Z[8];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        double2 lo = odd ? Y[q] : X[p][q];
-        double2 hi = odd ? X[p][4 + q] : Y[q];
-        dit(lo, hi, w3[q]);
-        Z[q] = lo;
-        Z[4 + q] = hi;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) X[p][q] = Z[q];
-    }
+        dit4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w4[r][0], w4[r][1], w4[r][2]);
   }
-#if LVB_TW_EARLY
+  // L_B -> L_A (cross-warp); pass A': radix-2 stage 2 on x7 = r0 (j = t),
+  // radix-4 (1,0) on (x8, x9) = (r1, r2), j = t + 128 r0
   const double2 w2 = tws(tw, 2, t);
 #pragma unroll
   for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 0, m + 1, t + 128 * r);
-#endif
-  // B' -> A crosses warps; B' writes stay in this warp's block, which other
-  // warps stopped reading at the (warp-local) exchange above
-  xchg<P>(
-      X, buf,
-      [&](int r) { return 64 * (b & ~1u) + u + 8 * ((r & 3) + 4 * odd) + 64 * (r >> 2); },
-      [&](int r) { return t + 128 * r; });
-  {
-    // stage 2, radix-4 (1,0) with j = t + 128 r
-#if !LVB_TW_EARLY
-    const double2 w2 = tws(tw, 2, t);
-#endif
+    for (int m = 0; m < 3; ++m) w4[r][m] = tw4(tw, 0, m + 1, t + 128 * r);
+  bar.sync();
+  xchg_cta<P, NB>(X, buf, bar, [&](int r) { return 16u * r + 128u * (L & 1) + u + 256u * w; },
+                  [&](int r) { return t + 128u * r; });
 #pragma unroll
-    for (int p = 0; p < P; ++p)
+  for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w2);
-#if !LVB_TW_EARLY
-    double2 w[2][3];
+    for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w2);
+#pragma unroll
+  for (int p = 0; p < P; ++p)
 #pragma unroll
     for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int m = 0; m < 3; ++m) w[r][m] = tw4(tw, 0, m + 1, t + 128 * r);
-#endif
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int r = 0; r < 2; ++r)
-        dit4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w[r][0], w[r][1], w[r][2]);
-  }
+      dit4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w4[r][0], w4[r][1], w4[r][2]);
 }
 
 // f64 -> Z_{2^64}, identical to oracle f64_to_torus. (An integer-pipe

@@ -52,6 +52,10 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
 }
 
 // ------------------------------------------------------------------ BR
+__device__ __forceinline__ double2 opaque(double2 v) {
+  asm volatile("" : "+d"(v.x), "+d"(v.y));
+  return v;
+}
 // Output of one sample-extracted coefficient j (value v = a'_j or b') to
 // the item's BrOut: mode 0 writes the LWE (+ body_add * Delta on the body);
 // mode 1 is the fused cell epilogue (kernel.cpp:152-163): v = step, and
@@ -117,7 +121,7 @@ __device__ __forceinline__ double2 mac2(double2 d0, double2 b0, double2 d1, doub
 // evict-last policy: 1 / 2 / 3 / 4 / 5 / 6 / 7 / 8 groups 68.82 / 68.61 /
 // 68.33 / 68.22 / 67.92 / 68.43 / 67.94 / 67.95 ms.
 #ifndef LVB_BSK_EARLY
-#define LVB_BSK_EARLY 5
+#define LVB_BSK_EARLY 8
 #endif
 #ifndef LVB_BSK_EARLY_EXACT
 #define LVB_BSK_EARLY_EXACT 6  // exact-mask kernel (6 values per group): 2 / 3 / 4 / 5 / 6 / 8 groups 93.3 / 92.6 / 89.9 / 90.0 / 89.6 / 89.7 ms
@@ -129,6 +133,10 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
   uint64_t* acc = reinterpret_cast<uint64_t*>(smem);                   // [2][kN]
   double2* buf = reinterpret_cast<double2*>(smem + 2 * kN * 8);        // [kXchgBufs][kM]
   uint16_t* ms = reinterpret_cast<uint16_t*>(smem + 2 * kN * 8 + kXchgBufs * kM * 16);
+  __shared__ uint32_t tmem_slot;
+  constexpr uint32_t kTmemCols = kExact ? 128 : 64;  // P spectra x 32 columns (power of 2)
+  const uint32_t tmem = tmem_alloc(&tmem_slot, kTmemCols);
+  const uint32_t tm = tmem_warp_base(tmem);
   const uint32_t t = threadIdx.x;
   const uint32_t item = blockIdx.x;
   const uint32_t n = a.n;
@@ -156,7 +164,19 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
   const double2 tw_fine = __ldg(a.twist + t);  // twist of x = t + 128 r is fine[t] * coarse[r]
 // (formed, not loaded: a 1024-entry twist table read through L1 measured
 // 92 vs 72 ms per 4096 — the L1 data pipe is the scarcer resource)
-#define TWIST_R(r) ((r) == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]))
+// (recomputed at each use: the opaque copy keeps the compiler from hoisting
+// the 7 products out of the CMUX loop and spilling them to local memory)
+#ifndef LVB_TZ_REGS
+#define LVB_TZ_REGS 0  // 1: the 8 twist factors held in registers across the CMUX loop
+#endif
+#if LVB_TZ_REGS
+  double2 tzr[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) tzr[r] = r == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]);
+#define TWIST_R(r) (tzr[r])
+#else
+#define TWIST_R(r) ((r) == 0 ? tw_fine : cmul(opaque(tw_fine), c_twist_coarse[r]))
+#endif
   __syncthreads();
   uint64_t own[2][16];  // [poly][2 r + half]
 #pragma unroll
@@ -200,7 +220,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
     double2 bpre[kEarly][kExact ? 6 : 4];
     const double2* bsk_row =
         a.bskf + (size_t)i * (8 * (kExact ? 6 : 4) * 128) + t;
-    fft_forward<2>(X, buf, tw, t, [&] {
+    fft_forward<2>(X, buf, tw, t, tm, [&] {
 #pragma unroll
       for (int q = 0; q < kEarly; ++q)
 #pragma unroll
@@ -209,11 +229,11 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
     });
 #define BSK_AT(q, e, ptr) ((q) < kEarly ? bpre[(q) < kEarly ? (q) : 0][e] : ld_stream<true>(ptr))
 #else
-    fft_forward<2>(X, buf, tw, t);
+    fft_forward<2>(X, buf, tw, t, tm);
 #define BSK_AT(q, e, ptr) ld_stream<true>(ptr)
 #endif
 
-    // pointwise MAC against BSK_i (bins 8t + q), then the inverse transforms;
+    // pointwise MAC against BSK_i (spectrum slots (t, q)), then the inverse transforms;
     // untwist (conj(twist); the 1/M is pre-applied to the BSK), back to the
     // torus, accumulate into the owned coefficients and publish them
     if constexpr (kExact) {
@@ -233,8 +253,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         Z[1][q] = mac2(d0, l0, d1, l1);
         Z[2][q] = mac2(d1, b1, d0, b0);  // body output: row 1 first
       }
-      __syncwarp();  // the forward's last (warp-local) buffer reads precede the inverse's
-      fft_inverse_a<3>(Z, buf, tw, t);
+      fft_inverse_a<3>(Z, buf, tw, t, tm);
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const double2 tv = TWIST_R(r);
@@ -262,8 +281,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         X[0][q] = mac2(d0, b00, d1, b10);
         X[1][q] = mac2(d1, b11, d0, b01);  // output o: row o first
       }
-      __syncwarp();  // the forward's last (warp-local) buffer reads precede the inverse's
-      fft_inverse_a<2>(X, buf, tw, t);
+      fft_inverse_a<2>(X, buf, tw, t, tm);
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const double2 tv = TWIST_R(r);
@@ -295,9 +313,10 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
     br_output(o, a.pool, a.pool_stride, j,
               j == 0 ? acc[0] : (j == kN ? acc[kN] : (uint64_t)0 - acc[kN - j]));
   signal_done(a, item);
+  tmem_free(tmem, kTmemCols);
 }
 #ifndef LVB_BR_CTAS
-#define LVB_BR_CTAS 3  // resident CTAs per SM the register allocation targets
+#define LVB_BR_CTAS 2  // resident CTAs per SM the register allocation targets
 #endif
 __global__ void __launch_bounds__(128, LVB_BR_CTAS) blind_rotate_kernel(BrArgs a) {
   blind_rotate_body<false>(a);
@@ -335,6 +354,9 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
   cg::cluster_group cluster = cg::this_cluster();
   const uint32_t p = cluster.block_rank();
   __shared__ __align__(8) uint64_t inbox_full[2];  // my inbox buffers' arrival barriers
+  __shared__ uint32_t tmem_slot;
+  const uint32_t tmem = tmem_alloc(&tmem_slot, 64);  // up to 2 spectra in lockstep (exact mask CTA)
+  const uint32_t tm = tmem_warp_base(tmem);
   const uint32_t t = threadIdx.x;
   // shared::cluster addresses of the partner's inbox and its barriers
   uint32_t r_inbox, r_full;
@@ -395,7 +417,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
     const uint32_t rot = ms[i];
     if (rot == 0) continue;  // uniform across the pair: both skip
 
-    // this CMUX's BSK row (bins 8t + q, output p), in flight during the
+    // this CMUX's BSK row (slots (t, q), output p), in flight during the
     // forward FFT: row p (this CTA's own polynomial) and row 1 - p
     double2 b_own[8], b_oth[8];
     if constexpr (!kExact) {
@@ -421,7 +443,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
       }
       X[0][r] = cmul(make_double2((double)d[0], (double)d[1]), tz[r]);
     }
-    fft_forward<1>(X, buf, tw, t);
+    fft_forward<1, 1>(X, buf, tw, t, tm);
     const uint32_t my_full = (uint32_t)__cvta_generic_to_shared(&inbox_full[parity]);
     if (t == 0)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(my_full),
@@ -469,8 +491,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
           Z[0][q] = mac2(X[0][q], ld_stream(bq), d1, ld_stream(bq + 384));
           Z[1][q] = mac2(X[0][q], ld_stream(bq + 128), d1, ld_stream(bq + 512));
         }
-        __syncwarp();  // the forward's last (warp-local) buffer reads precede the inverse's
-        fft_inverse_a<2>(Z, buf, tw, t);
+        fft_inverse_a<2, 1>(Z, buf, tw, t, tm);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const double2 ut = make_double2(tz[r].x, -tz[r].y);
@@ -487,8 +508,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
           const double2* bq = bsk + q * (6 * 128);
           X[0][q] = mac2(X[0][q], ld_stream(bq + 640), other_spec[q * 128 + t], ld_stream(bq + 256));
         }
-        __syncwarp();
-        fft_inverse_a<1>(X, buf, tw, t);
+        fft_inverse_a<1, 1>(X, buf, tw, t, tm);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const double2 ut = make_double2(tz[r].x, -tz[r].y);
@@ -502,8 +522,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
       }
       continue;
     }
-    __syncwarp();  // the forward's last (warp-local) buffer reads precede the inverse's
-    fft_inverse_a<1>(X, buf, tw, t);  // its barriers also order the rotated reads before the update
+    fft_inverse_a<1, 1>(X, buf, tw, t, tm);  // its barriers also order the rotated reads before the update
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const double2 ut = make_double2(tz[r].x, -tz[r].y);
@@ -527,6 +546,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
   for (uint32_t j = j0; j < j1; j += 128)
     br_output(o, a.pool, a.pool_stride, j, j == 0 || j == kN ? acc[0] : (uint64_t)0 - acc[kN - j]);
   signal_done(a, item);
+  tmem_free(tmem, 64);
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
@@ -791,7 +811,7 @@ __global__ void keygen_bsk_kernel(uint64_t seed, uint32_t noise_log2, const uint
 // accumulated error — a third of the external product's FFT error
 // (DESIGN.md §2). Operation order = oracle forward_i64_dd (bit-exact).
 // One CTA of 512 threads per polynomial (i, r, o), 32 KB of shared memory;
-// output in the MAC layout [i][q*4 + r*2 + o][t] for bin f = 8t + q,
+// output in the MAC layout [i][q*4 + r*2 + o][t] for position f = spec_pos(t, q),
 // pre-scaled by 2^-10 (exact).
 struct dd_t {
   double hi, lo;
@@ -859,8 +879,9 @@ bsk_fourier_kernel(const uint64_t* polys, uint32_t nouts, const double4* __restr
   }
   for (uint32_t f = t; f < kM; f += blockDim.x) {
     const double re = __dadd_rn(x[f].re.hi, x[f].re.lo), im = __dadd_rn(x[f].im.hi, x[f].im.lo);
-    bskf[(size_t)i * (8 * kRows * nouts * 128) + ((f & 7) * kRows * nouts + r * nouts + o) * 128 +
-         (f >> 3)] = make_double2(__dmul_rn(re, 0x1p-10), __dmul_rn(im, 0x1p-10));
+    const uint32_t sl = spec_slot(f);  // thread sl >> 3, register sl & 7 of the spectrum layout
+    bskf[(size_t)i * (8 * kRows * nouts * 128) + ((sl & 7) * kRows * nouts + r * nouts + o) * 128 +
+         (sl >> 3)] = make_double2(__dmul_rn(re, 0x1p-10), __dmul_rn(im, 0x1p-10));
   }
 }
 
@@ -885,6 +906,8 @@ __global__ void __launch_bounds__(128)
 fft_forward_debug_kernel(const int64_t* poly, const double2* __restrict__ tw,
                          const double2* __restrict__ twist, double2* spec) {
   __shared__ double2 buf[kM];
+  __shared__ uint32_t tmem_slot;
+  const uint32_t tmem = tmem_alloc(&tmem_slot, 32);
   const uint32_t t = threadIdx.x;
   double2 X[1][8];
 #pragma unroll
@@ -892,21 +915,23 @@ fft_forward_debug_kernel(const int64_t* poly, const double2* __restrict__ tw,
     const uint32_t x = t + 128 * q;
     X[0][q] = cmul(make_double2((double)poly[x], (double)poly[x + kM]), twist_at(twist, x));
   }
-  fft_forward<1>(X, buf, tw, t);
+  fft_forward<1, 1>(X, buf, tw, t, tmem_warp_base(tmem));
 #pragma unroll
-  for (int q = 0; q < 8; ++q) spec[8 * t + q] = X[0][q];
+  for (int q = 0; q < 8; ++q) spec[spec_pos(t, q)] = X[0][q];
+  tmem_free(tmem, 32);
 }
 
 __global__ void __launch_bounds__(128)
 fft_backward_debug_kernel(const double2* spec, const double2* __restrict__ tw,
                           const double2* __restrict__ twist, uint64_t* poly) {
   __shared__ double2 buf[kM];
+  __shared__ uint32_t tmem_slot;
+  const uint32_t tmem = tmem_alloc(&tmem_slot, 32);
   const uint32_t t = threadIdx.x;
   double2 X[1][8];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) X[0][q] = spec[8 * t + q];
-  __syncthreads();
-  fft_inverse_a<1>(X, buf, tw, t);
+  for (int q = 0; q < 8; ++q) X[0][q] = spec[spec_pos(t, q)];
+  fft_inverse_a<1, 1>(X, buf, tw, t, tmem_warp_base(tmem));
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const uint32_t x = t + 128 * r;
@@ -916,6 +941,7 @@ fft_backward_debug_kernel(const double2* spec, const double2* __restrict__ tw,
     poly[x] = f64_to_torus(z.x);
     poly[x + kM] = f64_to_torus(z.y);
   }
+  tmem_free(tmem, 32);
 }
 
 // FP64 pipe peak microbenchmark: 8 independent DFMA chains per thread.

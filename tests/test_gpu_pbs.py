@@ -273,3 +273,21 @@ def test_contexts_of_different_n_coexist(ctx, orc, golden):
         assert np.array_equal(ctx.pbs_host(rows, [ctx.lut(lut)] * 3), want)
     finally:
         small.close()
+
+
+def test_pbs_bit_exact_throughput_kernel(orc, golden, monkeypatch):
+    # waves above br_pair_max run the one-CTA-per-item throughput kernel
+    # (blind_rotate_kernel); 301 items = several CTAs per SM, a partial wave
+    monkeypatch.setenv("LVB_BR_PAIR_MAX", "0")
+    c = L.Context(seed=0)
+    names = ["identity", "minlut-negated", "eqlut9"]
+    luts = np.array([golden["luts"][n] for n in names], np.int32)
+    ids = np.array([c.lut(l) for l in luts], np.uint32)
+    count = 301
+    xs = (np.arange(count) * 7) % 32
+    rows = np.stack([orc.encrypt(int(x), 5000 + i) for i, x in enumerate(xs)])
+    which = np.arange(count) % len(names)
+    got = c.pbs_host(rows, ids[which])
+    want = orc.pbs_batch(rows, luts[which])
+    assert np.array_equal(got, want)
+    c.close()
