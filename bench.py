@@ -153,7 +153,21 @@ def cpu_oracle_pbs_rate(sample: int, threads: int = 0):
     dt = time.perf_counter() - t0
     ok = all(o.decrypt(out[i]) == vals[i] for i in range(sample))
     cores = threads if threads > 0 else (os.cpu_count() or 1)
-    return sample / dt, cores, dt, ok
+    return sample / dt, cores, dt, ok, rows, out
+
+
+TFHE_RS_MS_PER_PBS_CORE = 14.7  # paper-derived
+
+
+def cpu_context(cores: int, port_rate: float):
+    """What the scalar port is NOT: an optimised CPU TFHE library. The paper's
+    TFHE-rs v0.7.2 figure (~14.7 ms per PBS per core) scaled to the same
+    cores, so the GPU/port ratio is not read as the real speed-up."""
+    rs = cores * 1e3 / TFHE_RS_MS_PER_PBS_CORE
+    return {"tfhe_rs_paper_derived_pbs_per_s": rs, "cores": cores,
+            "port_vs_tfhe_rs": port_rate / rs,
+            "note": "14.7 ms/PBS/core derived from the paper's TFHE-rs timings (SURVEY §8d); "
+                    "not measured here (TFHE-rs is Rust, absent from this image)"}
 
 
 def reference_sim_rate():
@@ -216,7 +230,7 @@ def run_reference(args, ws, rank):
         cpu_oracle_pbs_rate(min(sample, 16), threads)
     rates = []
     for _ in range(args.steps):
-        r, cores, dt, ok = cpu_oracle_pbs_rate(sample, threads)
+        r, cores, dt, ok, _, _ = cpu_oracle_pbs_rate(sample, threads)
         rates.append(r)
     v = statistics.median(rates)
     line = {
@@ -231,6 +245,7 @@ def run_reference(args, ws, rank):
                                    "(oracle/tfhe_oracle.c, the CPU restatement; the reference's "
                                    "SimBackend performs no cryptography, see reference_sim)"},
         "e2e": {"value": v, "unit": "PBS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "context": cpu_context(threads, v),
         "reference_sim": reference_sim_rate(),
     }
     print(json.dumps(line), flush=True)
@@ -254,10 +269,30 @@ def phase_noise(ctx, out, vals):
             "ratio_std_err": float(np.sqrt(2.0 / e.size)) * v / ex}
 
 
+REPORT_FIELDS = ("distance", "visited_cells", "pbs_total", "pbs_equality", "pbs_kernel",
+                 "refresh_count", "preprocessing_pbs", "max_key_variance", "linear_ops",
+                 "half_width")
+
+
+def golden_configs():
+    """The compiled reference's RunReports for the five configs
+    (tests/golden/reference_runs.json, written by tests/golden/make_golden.py
+    from oracle/_ref; committed, so it travels to the GPU box)."""
+    with open(os.path.join(ROOT, "tests", "golden", "reference_runs.json")) as f:
+        return json.load(f)["configs"]
+
+
+def report_matches(got, want):
+    """Every RunReport counter of `got` equals the reference's `want`."""
+    return all(got[f] == want[f] for f in REPORT_FIELDS)
+
+
 def dp_cells(ctx, full_cfg5: bool = False):
-    """Encrypted DP cells/s through compute() (encrypt -> GPU traversal -> decrypt)."""
+    """Encrypted DP cells/s through compute() (encrypt -> GPU traversal -> decrypt).
+    Every run is checked against the compiled reference's report, pair by pair."""
     import paper_2508_14568_b200 as L
     from paper_2508_14568_b200 import workloads as W
+    gold = golden_configs()
     out = {}
     for name, fn, kw in (("cfg1", W.cfg1, {}), ("cfg3", W.cfg3, {}),
                          ("cfg4", W.cfg4, {"encoding": "dna4", "preprocess": True})):
@@ -268,7 +303,10 @@ def dp_cells(ctx, full_cfg5: bool = False):
         dt = time.perf_counter() - t0
         out[name] = {"cells": r["visited_cells"], "pbs": r["pbs_total"], "seconds": dt,
                      "cells_per_s": r["visited_cells"] / dt, "pbs_per_s": r["pbs_total"] / dt,
-                     "distance": r["distance"], "waves": r["waves"]}
+                     "distance": r["distance"], "waves": r["waves"],
+                     "reference_distance": gold[name]["report"]["distance"],
+                     "distances_ok": r["distance"] == gold[name]["report"]["distance"],
+                     "report_equals_reference": report_matches(r, gold[name]["report"])}
     # database scan: cfg4's encrypted query, one equality table built once,
     # against 64 plaintext server strings (cfg4's b and 63 more mutations)
     a, b = W.cfg4()
@@ -306,10 +344,15 @@ def dp_cells(ctx, full_cfg5: bool = False):
     cells = sum(r["visited_cells"] for r in reps)
     pbs = sum(r["pbs_total"] for r in reps)
     key = "cfg5" if full_cfg5 else "cfg5_subset16"
+    want = gold["cfg5"][:npairs]
     out[key] = {"pairs": npairs, "cells": cells, "pbs": pbs, "seconds": dt,
                 "cells_per_s": cells / dt, "pbs_per_s": pbs / dt,
                 "distances_sum": sum(r["distance"] for r in reps),
-                "reference_distances_sum": 4557 if full_cfg5 else None,
+                "reference_distances_sum": sum(w["report"]["distance"] for w in want),
+                "distances_ok": all(r["distance"] == w["report"]["distance"]
+                                    for r, w in zip(reps, want)),
+                "reports_equal_reference": sum(report_matches(r, w["report"])
+                                               for r, w in zip(reps, want)),
                 "note": "end to end through compute_batch(): encrypt both strings of every "
                         "pair on the GPU, all pairs' anti-diagonals per launch, decrypt"}
     return out
@@ -421,10 +464,19 @@ def main():
             line["dp_cells"] = {"error": repr(e)}
         try:
             sample = min(4096, 64 * (os.cpu_count() or 1))  # ~10 s of host work
-            r, cores, dt, ok = cpu_oracle_pbs_rate(sample)
+            r, cores, dt, ok, rows_o, out_o = cpu_oracle_pbs_rate(sample)
+            # the same ciphertexts through the product path (C ABI, host
+            # buffers): every output LWE must equal the oracle's bit for bit
+            got = ctx.pbs_host(rows_o, np.full(sample, lid, np.uint32))
+            same = int(np.sum(np.all(got == out_o, axis=1)))
             line["cpu_baseline"] = {"value": r, "unit": "PBS/s", "cores": cores, "kind": "port",
                                     "sample": f"{sample} of the 4096 cfg2 PBS on {cores} threads "
-                                              f"in {dt:.1f}s (oracle/tfhe_oracle.c), correct={ok}"}
+                                              f"in {dt:.1f}s (oracle/tfhe_oracle.c), correct={ok}",
+                                    "bit_exact": f"{same}/{sample}",
+                                    "context": cpu_context(cores, r),
+                                    "bit_exact_note": "GPU PBS outputs (lv_pbs_batch_host) on the "
+                                                      "oracle's own encryptions vs the oracle's "
+                                                      "outputs, every 2049-word LWE compared"}
         except Exception as e:
             line["cpu_baseline"] = {"error": repr(e)}
         # DP cells/s of the CPU port at the same bootstraps per cell (the

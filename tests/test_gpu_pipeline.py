@@ -62,13 +62,19 @@ def test_config4_preprocessed(golden):
         assert got[f] == golden["configs"]["cfg4"]["report"][f], f
 
 
-def test_config5_subset_batched(golden):
-    pairs = W.cfg5(8)
+def test_config5_full_batch(golden):
+    """BASELINE configs[4] in full: all 256 pairs (128 x 128 printable ASCII,
+    15% edits) in one compute_batch() wavefront (cli.cpp:164-210 batch mode,
+    acceptance criterion 11). Every pair's decrypted distance and every
+    RunReport counter equal the compiled reference's (golden cfg5). ~4 min."""
+    pairs = W.cfg5(256)
     reps = L.compute_batch(pairs)
-    for rep, want in zip(reps, golden["configs"]["cfg5"][:8]):
-        for f in ("distance", "visited_cells", "pbs_equality", "pbs_kernel", "pbs_total",
-                  "refresh_count", "max_key_variance"):
-            assert rep[f] == want["report"][f], f
+    assert len(reps) == 256
+    for i, (rep, want) in enumerate(zip(reps, golden["configs"]["cfg5"])):
+        assert (want["a"], want["b"]) == pairs[i]
+        for f in FIELDS:
+            assert rep[f] == want["report"][f], (i, f, rep[f], want["report"][f])
+    assert sum(r["distance"] for r in reps) == 4557
 
 
 def test_empty_operands():
