@@ -103,8 +103,10 @@ void lv_ctx_destroy(lv_ctx* ctx);
  * holds the secret keys; lv_keys_export copies its evaluation keys to host
  * buffers of lv_keys_size words — the BSK in the standard domain,
  * [i < n][row < 2][poly < 2][N] u64 (GGSW rows of s_i under the GLWE key),
- * and the KSK [j < N][level < 5][n + 1] u64 — plus the key-set id (the
- * generating seed) that LEQT tables carry. lv_ctx_create_eval builds an
+ * and the KSK [j < N][level < 5][n + 1] u64 — plus the key-set id that
+ * LEQT tables carry: a fingerprint of the public KSK and the parameter set,
+ * never the generating seed (a server given a non-zero key_id that does not
+ * match the keys it received fails with LV_ERR_INVALID_PARAMS). lv_ctx_create_eval builds an
  * evaluation-only context from them (the Fourier BSK is computed on the
  * device): every homomorphic entry point works, while lv_encrypt,
  * lv_decrypt, lv_phase and the secret parts of lv_debug_keys fail with
@@ -115,6 +117,8 @@ int lv_keys_size(const lv_params* params, uint64_t* bsk_count, uint64_t* ksk_cou
 int lv_keys_export(lv_ctx* ctx, uint64_t* bsk, uint64_t* ksk, uint64_t* key_id);
 int lv_ctx_create_eval(const lv_params* params, const uint64_t* bsk, const uint64_t* ksk,
                        uint64_t key_id, lv_ctx** out);
+/* The key-set fingerprint of any context (client or server). */
+int lv_ctx_key_id(lv_ctx* ctx, uint64_t* key_id);
 const char* lv_last_error(void);
 int lv_abi_version(void);
 

@@ -14,6 +14,7 @@
 #include <string>
 #include <utility>
 #include <memory>
+#include <random>
 #include <vector>
 
 #include "leuven_b200.h"
@@ -63,10 +64,18 @@ struct StatsSnapshot {  // backend.hpp:36-40
 
 // The GPU backend: same operations as leuven::Backend (backend.hpp:54-76),
 // each also available in batched form.
+// Key seeds default to OS entropy; pass a fixed seed only for tests and
+// reproducible experiments (every secret derives from it).
+inline uint64_t random_seed() {
+  std::random_device rd;
+  return ((uint64_t)rd() << 32) ^ rd();
+}
+
 class GpuBackend {
  public:
   // exact_mask_product: see lv_params (noise of exact products, 1.4x time)
-  explicit GpuBackend(double budget = 4000.0, uint64_t seed = 0, bool exact_mask_product = false) {
+  explicit GpuBackend(double budget = 4000.0, uint64_t seed = random_seed(),
+                      bool exact_mask_product = false) {
     lv_params p;
     lv_default_params(&p);
     p.max_variance_budget = budget;

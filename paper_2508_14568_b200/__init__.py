@@ -113,7 +113,7 @@ class Run(ctypes.Structure):
 # Every exported symbol declared in include/leuven_b200.h (checked by tests).
 EXPORTS = [
     "lv_default_params", "lv_ctx_create", "lv_ctx_destroy", "lv_last_error", "lv_abi_version",
-    "lv_keys_size", "lv_keys_export", "lv_ctx_create_eval",
+    "lv_keys_size", "lv_keys_export", "lv_ctx_create_eval", "lv_ctx_key_id",
     "lv_lut_table", "lv_encrypt", "lv_trivial", "lv_decrypt", "lv_add", "lv_sub", "lv_scalar_mul",
     "lv_scalar_add", "lv_lut_upload", "lv_pbs_batch", "lv_refresh_batch", "lv_predict_variance",
     "lv_get_stats", "lv_get_params", "lv_release", "lv_ledger_variance", "lv_export",
@@ -150,6 +150,7 @@ def lib():
             "lv_keys_size": (ctypes.c_int, [P(Params), P(u64), P(u64)]),
             "lv_keys_export": (ctypes.c_int, [vp, P(u64), P(u64), P(u64)]),
             "lv_ctx_create_eval": (ctypes.c_int, [P(Params), P(u64), P(u64), u64, P(vp)]),
+            "lv_ctx_key_id": (ctypes.c_int, [vp, P(u64)]),
             "lv_ctx_destroy": (None, [vp]),
             "lv_last_error": (ctypes.c_char_p, []),
             "lv_abi_version": (ctypes.c_int, []),
@@ -270,8 +271,12 @@ class Context:
     scalars or arrays and is batched underneath.
     """
 
-    def __init__(self, seed: int = 0, params: Params | None = None, budget: float | None = None,
-                 _eval_keys=None, device: int | None = None):
+    def __init__(self, seed: int | None = None, params: Params | None = None,
+                 budget: float | None = None, _eval_keys=None, device: int | None = None):
+        # every secret derives from the seed: OS entropy unless a test or an
+        # experiment pins it
+        if seed is None:
+            seed = int.from_bytes(os.urandom(8), "little")
         p = params if params is not None else default_params()
         if budget is not None:
             p.max_variance_budget = float(budget)
@@ -304,6 +309,12 @@ class Context:
         _check(lib().lv_keys_export(self._h, _ptr(bsk, ctypes.c_uint64), _ptr(ksk, ctypes.c_uint64),
                                     ctypes.byref(kid)))
         return bsk, ksk, kid.value
+
+    def key_id(self) -> int:
+        """Key-set fingerprint (hash of the public KSK + parameters)."""
+        k = ctypes.c_uint64()
+        _check(lib().lv_ctx_key_id(self._h, ctypes.byref(k)))
+        return k.value
 
     @classmethod
     def evaluation(cls, bsk, ksk, key_id: int, params: Params | None = None,
@@ -358,6 +369,8 @@ class Context:
 
     def _lin2(self, fn, a, b):
         a, b = _u32(a), _u32(b)
+        if a.size != b.size:
+            raise InvalidParams(f"operand counts differ ({a.size} vs {b.size})")
         out = np.zeros(a.size, np.uint32)
         _check(fn(self._h, _ptr(a, ctypes.c_uint32), _ptr(b, ctypes.c_uint32), a.size,
                   _ptr(out, ctypes.c_uint32)))

@@ -560,6 +560,29 @@ int lv_lut_table(int32_t which, int32_t* out16) {
   });
 }
 
+// Key-set fingerprint from PUBLIC material only: FNV-1a over the
+// parameter set and the first 8192 words of the key-switching key (its
+// masks and bodies are public; the generating seed is never exported or
+// serialised). Client and server contexts of one key set agree on it.
+static uint64_t key_fingerprint(lv_ctx* c) {
+  constexpr size_t kWords = 8192;
+  std::vector<uint64_t> h(std::min<size_t>(kWords, ksk_words(c->p.n)));
+  LV_CUDA(cudaMemcpy(h.data(), c->d_ksk, h.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  uint64_t f = 0xcbf29ce484222325ull;
+  auto mix = [&](uint64_t v) {
+    for (int b = 0; b < 8; ++b) {
+      f ^= (v >> (8 * b)) & 0xff;
+      f *= 0x100000001b3ull;
+    }
+  };
+  mix(c->p.n);
+  mix(c->p.N);
+  mix(c->p.k);
+  mix(c->p.exact_mask_product);
+  for (uint64_t v : h) mix(v);
+  return f;
+}
+
 static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bsk,
                       const uint64_t* ksk, uint64_t key_id, lv_ctx** out) {
   return guard([&] {
@@ -588,7 +611,6 @@ static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bs
     try {
       c->p = p;
       c->seed = seed;
-      c->key_id = key_id;
       LV_CUDA(cudaGetDevice(&c->device));
       LV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       LV_CUDA(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
@@ -632,6 +654,10 @@ static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bs
         load_eval_keys(c, bsk, ksk);
       else
         keygen(c);
+      c->key_id = key_fingerprint(c);
+      // a server context checks the client's announced fingerprint
+      if (bsk && key_id != 0 && key_id != c->key_id)
+        throw Error(LV_ERR_INVALID_PARAMS, "evaluation keys do not match the announced key id");
       c->min_lut[0] = lut_id(c, min_lut_entries(false));
       c->min_lut[1] = lut_id(c, min_lut_entries(true));
       std::array<int32_t, 16> id{};
@@ -647,7 +673,7 @@ static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bs
 }
 
 int lv_ctx_create(const lv_params* params, uint64_t seed, lv_ctx** out) {
-  return create_ctx(params, seed, nullptr, nullptr, seed, out);
+  return create_ctx(params, seed, nullptr, nullptr, 0, out);
 }
 
 int lv_ctx_create_eval(const lv_params* params, const uint64_t* bsk, const uint64_t* ksk,
@@ -680,6 +706,10 @@ int lv_keys_export(lv_ctx* c, uint64_t* bsk, uint64_t* ksk, uint64_t* key_id) {
     }
     if (key_id) *key_id = c->key_id;
   });
+}
+
+int lv_ctx_key_id(lv_ctx* c, uint64_t* key_id) {
+  return guard([&] { *key_id = c->key_id; });
 }
 
 void lv_ctx_destroy(lv_ctx* c) {

@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -87,7 +88,7 @@ struct lv_eqtable {
 struct lv_ctx {
   lv_params p{};
   uint64_t seed = 0;
-  uint64_t key_id = 0;  // key-set fingerprint (the seed of the context that generated the keys)
+  uint64_t key_id = 0;  // key-set fingerprint: hash of public key material (key_fingerprint), never the seed
   cudaStream_t stream = nullptr;
   cudaStream_t copy_out = nullptr;  // lv_pbs_batch_host: chunk downloads behind the compute
   int device = 0;
@@ -134,7 +135,11 @@ struct lv_ctx {
   lvb::DevBuf<uint8_t> ks_digits;
   lvb::DevBuf<uint64_t> ks_body;
 
-  std::map<std::string, lvb::PairPlan> plan_cache;
+  // traversal plans per grid shape, LRU-bounded by total cells (a server
+  // scanning many string lengths must not grow it without limit); callers
+  // hold shared_ptrs, so eviction never invalidates a running traversal
+  std::map<std::string, std::pair<std::shared_ptr<const lvb::PairPlan>, uint64_t>> plan_cache;
+  uint64_t plan_cache_cells = 0, plan_cache_tick = 0;
   uint32_t min_lut[2] = {0, 0};
   uint32_t br_pair_max = 0;  // waves up to this size run blind_rotate_pair_kernel
   uint32_t br_slots = 0;     // blind-rotation CTAs resident on the whole GPU at once

@@ -545,7 +545,15 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
   const uint32_t j0 = p == 0 ? t : kN + t, j1 = p == 0 ? kN : kN + 1;
   for (uint32_t j = j0; j < j1; j += 128)
     br_output(o, a.pool, a.pool_stride, j, j == 0 || j == kN ? acc[0] : (uint64_t)0 - acc[kN - j]);
-  signal_done(a, item);
+  // one count per item: both CTAs' output stores are ordered (cluster
+  // barrier, release/acquire) before rank 0 fences them to device scope
+  if (a.done) {
+    cluster.sync();
+    if (p == 0 && t == 0) {
+      __threadfence();
+      atomicAdd(a.done + item / a.done_chunk, 1u);
+    }
+  }
   tmem_free(tmem, 64);
 }
 

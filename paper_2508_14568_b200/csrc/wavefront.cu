@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <string>
@@ -50,8 +51,12 @@ static BandSpec to_band(const lv_band* b) {
   return s;
 }
 
-static const PairPlan& get_plan(lv_ctx* c, uint32_t m, uint32_t n, const BandSpec& band,
-                                bool negated, double budget) {
+// Plan cache bound: ~24 B per cell, so 8M cells is ~200 MB of host memory.
+constexpr uint64_t kPlanCacheCells = 8u << 20;
+
+static std::shared_ptr<const PairPlan> get_plan(lv_ctx* c, uint32_t m, uint32_t n,
+                                                const BandSpec& band, bool negated,
+                                                double budget) {
   if (!band.covers(m, n))
     throw Error(LV_ERR_BAND_TOO_NARROW, "band half-width " + std::to_string(band.half_width) +
                                             " below length difference");
@@ -61,8 +66,25 @@ static const PairPlan& get_plan(lv_ctx* c, uint32_t m, uint32_t n, const BandSpe
                           std::to_string(band.mode) + "/" + std::to_string(band.half_width) + "/" +
                           (negated ? "n" : "o") + "/" + std::to_string(budget);
   auto it = c->plan_cache.find(key);
-  if (it != c->plan_cache.end()) return it->second;
-  return c->plan_cache.emplace(key, plan_pair(m, n, band, negated, budget)).first->second;
+  if (it != c->plan_cache.end()) {
+    it->second.second = ++c->plan_cache_tick;
+    return it->second.first;
+  }
+  auto plan = std::make_shared<const PairPlan>(plan_pair(m, n, band, negated, budget));
+  const uint64_t cells = plan->cells.size() + 1;
+  // evict least recently used plans until the new one fits
+  while (!c->plan_cache.empty() && c->plan_cache_cells + cells > kPlanCacheCells) {
+    auto lru = c->plan_cache.begin();
+    for (auto e = c->plan_cache.begin(); e != c->plan_cache.end(); ++e)
+      if (e->second.second < lru->second.second) lru = e;
+    c->plan_cache_cells -= lru->second.first->cells.size() + 1;
+    c->plan_cache.erase(lru);
+  }
+  if (cells <= kPlanCacheCells) {
+    c->plan_cache.emplace(key, std::make_pair(plan, ++c->plan_cache_tick));
+    c->plan_cache_cells += cells;
+  }
+  return plan;
 }
 
 // One pair's traversal inputs.
@@ -93,6 +115,34 @@ static LinDesc lin(std::initializer_list<std::pair<uint32_t, int32_t>> terms, in
   return d;
 }
 
+// Budget check of the equality bootstraps (SimBackend::pbs,
+// backend.cpp:62-67, reached through eq4 / fold_step, equality.cpp:22-70):
+// stage 0 bootstraps x - y, stage s > 0 bootstraps 2 x_s - 2 y_s - eq_{s-1}
+// + 1 with eq_{s-1} a fresh PBS output (variance 1, its own source). A
+// bound from the per-stage maxima clears the common case (fresh symbols)
+// without touching pairs of cells; otherwise every visited cell's inputs
+// are checked exactly, before anything is launched.
+static void check_equality_budget(lv_ctx* c, const PairIn& in, const PairPlan& plan, uint32_t S,
+                                  double budget) {
+  for (uint32_t s = 0; s < S; ++s) {
+    const int32_t f = s == 0 ? 1 : 2;
+    const int64_t extra = s == 0 ? 0 : 1;
+    int64_t va = 0, vb = 0;
+    for (uint32_t i = 0; i < in.m; ++i) va = std::max(va, c->ledgers[in.a[(size_t)i * S + s]].variance());
+    for (uint32_t j = 0; j < in.n; ++j) vb = std::max(vb, c->ledgers[in.b[(size_t)j * S + s]].variance());
+    const double bound = std::pow(f * (std::sqrt((double)va) + std::sqrt((double)vb)), 2) + extra;
+    if (bound <= budget) continue;
+    for (const CellPlan& cell : plan.cells) {
+      const NoiseLedger& x = c->ledgers[in.a[(size_t)(cell.i - 1) * S + s]];
+      const NoiseLedger& y = c->ledgers[in.b[(size_t)(cell.j - 1) * S + s]];
+      const int64_t v = combined_variance(x, f, y, -f) + extra;
+      if ((double)v > budget)
+        throw Error(LV_ERR_NOISE_BUDGET, "equality bootstrap input variance " + std::to_string(v) +
+                                             " exceeds budget " + std::to_string(budget));
+    }
+  }
+}
+
 // Runs a batch of traversals (S = symbols per character; S == 0 selects
 // the preprocessed mode with eq9 taken from the pair's table).
 static void run_traversals(lv_ctx* c, const std::vector<PairIn>& pairs, uint32_t S, bool negated,
@@ -106,10 +156,11 @@ static void run_traversals(lv_ctx* c, const std::vector<PairIn>& pairs, uint32_t
   }
   const int32_t dv_coef = negated ? -1 : 1;
 
-  std::vector<const PairPlan*> plans(pairs.size());
+  std::vector<std::shared_ptr<const PairPlan>> plans(pairs.size());
   for (size_t p = 0; p < pairs.size(); ++p) {
     const PairIn& in = pairs[p];
-    plans[p] = &get_plan(c, in.m, in.n, in.band, negated, budget);
+    plans[p] = get_plan(c, in.m, in.n, in.band, negated, budget);
+    if (S > 0) check_equality_budget(c, in, *plans[p], S, budget);
     if (in.table) {
       for (uint32_t j = 0; j < in.n; ++j)
         if (!in.table->rows.count(in.plain[j]))
@@ -435,6 +486,16 @@ int lv_eq_table_build(lv_ctx* c, const lv_ct* a, size_t m, uint32_t S, const cha
     check_handles(c, a, m * S);
     const uint32_t lut_eq1 = lut_id(c, eq_lut_entries(1));
     const uint32_t lut_eq9 = lut_id(c, eq_lut_entries(9));
+    // budget check of every equality bootstrap input (x - y_const at stage
+    // 0, 2 x_s - eq_{s-1} + const after it), as SimBackend::pbs would throw
+    for (size_t i = 0; i < m; ++i)
+      for (uint32_t s = 0; s < S; ++s) {
+        const int64_t v = c->ledgers[a[i * S + s]].variance() * (s == 0 ? 1 : 4) + (s == 0 ? 0 : 1);
+        if ((double)v > c->p.max_variance_budget)
+          throw Error(LV_ERR_NOISE_BUDGET, "equality bootstrap input variance " + std::to_string(v) +
+                                               " exceeds budget " +
+                                               std::to_string(c->p.max_variance_budget));
+      }
     auto* t = new lv_eqtable();
     t->length = m;
     try {

@@ -243,7 +243,12 @@ def distance_encrypted(ctx: Context, a: EncryptedString, b: EncryptedString, ban
 
 def distance_batch(ctx: Context, pairs, bands, encoding: str = "negated"):
     """All pairs' same-index anti-diagonals share one launch."""
-    S = next((p[0].chars.shape[1] for p in pairs if p[0].chars.size), 2)
+    # symbols per character from the arrays' shape (empty strings keep (0, S));
+    # every operand must agree, or C would read past the shorter buffers
+    shapes = {p[k].chars.shape[1] for p in pairs for k in (0, 1) if p[k].chars.ndim == 2}
+    if len(shapes) > 1:
+        raise InvalidParams("equality operands must have the same nonzero symbol count")
+    S = shapes.pop() if shapes else 2
     A = np.concatenate([_u32(p[0].chars) for p in pairs]) if pairs else np.zeros(0, np.uint32)
     B = np.concatenate([_u32(p[1].chars) for p in pairs]) if pairs else np.zeros(0, np.uint32)
     a_off = np.zeros(len(pairs) + 1, np.uint64)
@@ -380,7 +385,7 @@ def _resolve_band(mode: str, ell, m: int, n: int) -> BandSpec:
 _CTX_CACHE: dict = {}
 
 
-def _context(seed: int, budget: float) -> Context:
+def _context(seed: int | None, budget: float) -> Context:
     key = (seed, float(budget))
     if key not in _CTX_CACHE:
         _CTX_CACHE[key] = Context(seed=seed, budget=budget)
@@ -389,7 +394,7 @@ def _context(seed: int, budget: float) -> Context:
 
 def compute(a: str, b: str, mode: str = "exact", ell=None, encoding: str = "ascii7",
             budget: float = 4000.0, key_encoding: str = "negated", preprocess: bool = False,
-            ctx: Context | None = None, seed: int = 0, include_timing: bool = False) -> dict:
+            ctx: Context | None = None, seed: int | None = None, include_timing: bool = False) -> dict:
     """cli::compute_report (cli.cpp:53-91) / bindings compute(): encrypt ->
     traverse on the GPU -> decrypt; counters as in RunReport (cli.hpp:25-37)."""
     import time
@@ -436,7 +441,7 @@ def compute(a: str, b: str, mode: str = "exact", ell=None, encoding: str = "asci
 
 
 def compute_batch(pairs, encoding: str = "ascii7", budget: float = 4000.0,
-                  key_encoding: str = "negated", ctx: Context | None = None, seed: int = 0):
+                  key_encoding: str = "negated", ctx: Context | None = None, seed: int | None = None):
     """Batch mode (cli.cpp:164-210): exact band, one report per pair, all
     pairs traversed together on the GPU."""
     spec = AlphabetSpec.by_name(encoding)
@@ -478,7 +483,7 @@ def report_json(report: dict, include_timing: bool = False) -> str:
 
 def run_batch(lines, mode: str = "exact", ell=None, encoding: str = "ascii7",
               budget: float = 4000.0, key_encoding: str = "negated", preprocess: bool = False,
-              ctx: Context | None = None, seed: int = 0):
+              ctx: Context | None = None, seed: int | None = None):
     """cli::run_batch (cli.cpp:164-210): one JSON object {"a":..,"b":..} per
     line -> one report line (or {"error": ...}) per line, input order kept.
     All valid lines of a non-preprocessed batch are traversed together: every

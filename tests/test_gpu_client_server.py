@@ -23,7 +23,7 @@ def split():
 
 def test_exported_keys_equal_oracle(ctx, orc):
     bsk, ksk, kid = ctx.export_keys()
-    assert kid == 0
+    assert kid not in (0, 1)  # a fingerprint of public material, never the seed (0 here)
     assert np.array_equal(ksk, orc.ksk())
     assert np.array_equal(bsk, orc.bsk())
 
@@ -39,6 +39,22 @@ def test_server_has_no_secret(split):
         server.export_keys()
     with pytest.raises(L.InvalidParams):
         L.Context.evaluation(np.zeros(10, np.uint64), np.zeros(10, np.uint64), 0)
+
+
+def test_key_id_is_public_fingerprint(split):
+    """the key id must not be the generating seed (anyone holding
+    a table file could regenerate the secret key from it). It is a hash of
+    the public KSK + parameters: equal on client and server, different per
+    key set, and a server rejects keys that do not match an announced id."""
+    client, server = split
+    bsk, ksk, kid = client.export_keys()
+    assert kid != 3
+    assert server.key_id() == kid
+    other = L.Context(seed=4)
+    assert other.export_keys()[2] != kid
+    other.close()
+    with pytest.raises(L.InvalidParams):
+        L.Context.evaluation(bsk, ksk, kid ^ 1)
 
 
 def test_server_pbs_bit_identical(split, golden):

@@ -66,3 +66,22 @@ def test_cell_all_18_inputs(ctx, golden, encoding):
     assert list(ctx.decrypt(step)) == want
     assert list(ctx.decrypt(ctx.sub(step, dh))) == [(w - h) % 32 for w, (_, h, _) in zip(want, combos)]
     assert list(ctx.decrypt(ctx.sub(step, dv))) == [(w - v) % 32 for w, (v, _, _) in zip(want, combos)]
+
+
+def test_equality_inputs_checked_against_budget(ctx):
+    """ADVICE r1: eq4 / fold_step go through SimBackend::pbs in the
+    reference (equality.cpp:22-70), which throws NoiseBudgetExceeded on an
+    over-noisy input. Symbols scaled by scalar_mul(64) (variance 4096 >
+    4000) must be rejected before anything is launched, in the traversal
+    and in the preprocessing table build; fresh symbols pass."""
+    spec = L.AlphabetSpec.ascii7()
+    xa = L.encrypt_string("ab", spec, ctx)
+    xb = L.encrypt_string("ac", spec, ctx)
+    bad = L.EncryptedString(ctx.scalar_mul(xa.chars.reshape(-1), 64).reshape(xa.chars.shape))
+    band = L.BandSpec.exact(2, 2)
+    with pytest.raises(L.NoiseBudgetExceeded):
+        L.distance_encrypted(ctx, bad, xb, band)
+    with pytest.raises(L.NoiseBudgetExceeded):
+        L.build_eq_table(ctx, bad, spec)
+    run = L.distance_encrypted(ctx, xa, xb, band)
+    assert int(ctx.decrypt([run.score])[0]) == 1
