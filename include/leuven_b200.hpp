@@ -82,6 +82,12 @@ class GpuBackend {
     p.exact_mask_product = exact_mask_product ? 1u : 0u;
     check(lv_ctx_create(&p, seed, &ctx_));
   }
+  // key-set fingerprint (hash of the public KSK + parameters; lv_ctx_key_id)
+  uint64_t key_id() const {
+    uint64_t k = 0;
+    check(lv_ctx_key_id(ctx_, &k));
+    return k;
+  }
   ~GpuBackend() { lv_ctx_destroy(ctx_); }
   GpuBackend(const GpuBackend&) = delete;
   GpuBackend& operator=(const GpuBackend&) = delete;

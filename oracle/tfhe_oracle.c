@@ -45,7 +45,8 @@ struct orc_ctx {
   double* bskf;    /* interleaved (re, im) */
   double* bskf_hi; /* exact_mask_product: spectra of H and Lo of every mask */
   double* bskf_lo; /* polynomial, [(i * rows + r) * k + q][2M]             */
-  double* tw;      /* W[t] = exp(-2 pi i t / M), t < M, interleaved */
+  double* fwd_lf;  /* forward twiddles (c, t), level s block b at 2^s - 1 + b */
+  double* inv_lf;  /* inverse twiddles (c, t) of conj(W^k), k < M/2 */
   double* twist;   /* zeta^j = exp(i pi j / N), j < M */
   double* untwist; /* zeta^-j / M */
   double* tw_dd;   /* W[t], t < M/2, as (re.hi, re.lo, im.hi, im.lo) */
@@ -229,115 +230,107 @@ static inline void cmul(double ar, double ai, double br, double bi, double* r, d
   *i = fma(ar, bi, t2);
 }
 
-/* The transform (M = 1024) is a fixed network (the GPU reorders data,
- * never arithmetic; csrc/fft.cuh): forward = DIF with radix-4 butterflies on
- * the stage pairs (0,1), (3,4), (6,7), (8,9) and radix-2 stages 2, 5;
- * inverse = its DIT mirror: radix-4 (9,8), (7,6), radix-2 5, radix-4 (4,3),
- * radix-2 2, radix-4 (1,0). Output of the forward / input of the inverse:
- * bit-reversed bin order. W^t = exp(-2 pi i t / M) from long double, t < M. */
+/* The transform (M = N/2 complex points) is a fixed network of radix-2
+ * Cooley-Tukey butterflies u +- w v, each in Linzer-Feig form: the twiddle
+ * w = c (1 + i t) is stored as (c, t) = (cos, tan) of its angle, rounded
+ * from long double, and the butterfly is six FMAs (ct_lf below).
+ * forward (fft_fwd): negacyclic, natural order in, bit-reversed out —
+ *   level s (half = M >> (s+1)), block b: w = zeta^e(s, b) with
+ *   e(s, b) = (M >> (s+1)) (1 - 4 brv_s(b)) mod 2N, zeta = exp(i pi / N);
+ *   the output is the spectrum of the twisted DFT (bin f = the polynomial
+ *   at zeta^(1 - 4 brv(f))), so no separate twist is applied. Sibling
+ *   blocks differ by w(s, 2b+1) = -i w(s, 2b): at the levels where the GPU
+ *   holds the block's low bit in registers (4, 5, 7, 9; production size)
+ *   an odd block uses its even sibling's (c, t) with the -i folded into
+ *   the FMA operands (ct_lf_mi), so one twiddle serves both.
+ * inverse (fft_inv): cyclic DIT, bit-reversed in, natural out — stage s =
+ *   logM-1 .. 0, pair (j, j + half), w = conj(W^k), k = j << s, W = exp(-2
+ *   pi i / M); the two stages with half <= 2 have w in {1, i} and are exact
+ *   additions (ct_one, ct_i); at stages 0, 1, 3, 4, 6 a pair with k >= M/4
+ *   uses conj(W^(k - M/4)) with the factor i folded in (ct_lf_i); the
+ *   untwist follows in backward_torus.
+ * Toy sizes (logM != 10) use the plain forms everywhere.
+ * The GPU (csrc/fft.cuh) reorders data, never arithmetic. */
 typedef struct {
   double re, im;
 } cpx;
-static inline cpx cadd(cpx a, cpx b) { return (cpx){a.re + b.re, a.im + b.im}; }
-static inline cpx csub(cpx a, cpx b) { return (cpx){a.re - b.re, a.im - b.im}; }
-static inline cpx cmulw(cpx a, const double* w) {
-  cpx r;
-  cmul(a.re, a.im, w[0], w[1], &r.re, &r.im);
-  return r;
-}
-static inline cpx cmulwc(cpx a, const double* w) {
-  cpx r;
-  cmul(a.re, a.im, w[0], -w[1], &r.re, &r.im);
-  return r;
-}
 static inline cpx ld(const double* x, uint32_t i) { return (cpx){x[2 * i], x[2 * i + 1]}; }
 static inline void st(double* x, uint32_t i, cpx v) {
   x[2 * i] = v.re;
   x[2 * i + 1] = v.im;
 }
 
-static void r2_dif(const orc_ctx* c, double* x, uint32_t s) {
-  const uint32_t M = c->M, half = M >> (s + 1);
-  for (uint32_t blk = 0; blk < M; blk += 2 * half)
-    for (uint32_t j = 0; j < half; ++j) {
-      const cpx u = ld(x, blk + j), v = ld(x, blk + j + half);
-      st(x, blk + j, cadd(u, v));
-      st(x, blk + j + half, cmulw(csub(u, v), c->tw + 2 * ((size_t)j << s)));
-    }
+static inline void ct_lf(double* x, uint32_t iu, uint32_t iv, const double* w /* c, t */) {
+  const cpx u = ld(x, iu), v = ld(x, iv);
+  const double a = fma(-w[1], v.im, v.re);
+  const double b = fma(w[1], v.re, v.im);
+  st(x, iu, (cpx){fma(w[0], a, u.re), fma(w[0], b, u.im)});
+  st(x, iv, (cpx){fma(-w[0], a, u.re), fma(-w[0], b, u.im)});
+}
+/* u +- (-i w) v with w = c (1 + i t): (-i w) v = c (b - i a) */
+static inline void ct_lf_mi(double* x, uint32_t iu, uint32_t iv, const double* w) {
+  const cpx u = ld(x, iu), v = ld(x, iv);
+  const double a = fma(-w[1], v.im, v.re);
+  const double b = fma(w[1], v.re, v.im);
+  st(x, iu, (cpx){fma(w[0], b, u.re), fma(-w[0], a, u.im)});
+  st(x, iv, (cpx){fma(-w[0], b, u.re), fma(w[0], a, u.im)});
+}
+/* u +- (i w) v: (i w) v = c (-b + i a) */
+static inline void ct_lf_i(double* x, uint32_t iu, uint32_t iv, const double* w) {
+  const cpx u = ld(x, iu), v = ld(x, iv);
+  const double a = fma(-w[1], v.im, v.re);
+  const double b = fma(w[1], v.re, v.im);
+  st(x, iu, (cpx){fma(-w[0], b, u.re), fma(w[0], a, u.im)});
+  st(x, iv, (cpx){fma(w[0], b, u.re), fma(-w[0], a, u.im)});
+}
+static inline void ct_one(double* x, uint32_t iu, uint32_t iv) { /* w = 1 */
+  const cpx u = ld(x, iu), v = ld(x, iv);
+  st(x, iu, (cpx){u.re + v.re, u.im + v.im});
+  st(x, iv, (cpx){u.re - v.re, u.im - v.im});
+}
+static inline void ct_i(double* x, uint32_t iu, uint32_t iv) { /* w = i: u +- i v */
+  const cpx u = ld(x, iu), v = ld(x, iv);
+  st(x, iu, (cpx){u.re - v.im, u.im + v.re});
+  st(x, iv, (cpx){u.re + v.im, u.im - v.re});
 }
 
-/* stages s, s+1: (x0, x1, x2, x3) at j + {0, H, 2H, 3H}, k = j << s */
-static void r4_dif(const orc_ctx* c, double* x, uint32_t s) {
-  const uint32_t M = c->M, H = M >> (s + 2);
-  for (uint32_t blk = 0; blk < M; blk += 4 * H)
-    for (uint32_t j = 0; j < H; ++j) {
-      const size_t k = (size_t)j << s;
-      const uint32_t i0 = blk + j;
-      const cpx x0 = ld(x, i0), x1 = ld(x, i0 + H), x2 = ld(x, i0 + 2 * H), x3 = ld(x, i0 + 3 * H);
-      const cpx A = cadd(x0, x2), B = cadd(x1, x3), C = csub(x0, x2), d = csub(x1, x3);
-      const cpx D = {d.im, -d.re}; /* (x1 - x3) * -i */
-      st(x, i0, cadd(A, B));
-      st(x, i0 + H, cmulw(csub(A, B), c->tw + 2 * (2 * k)));
-      st(x, i0 + 2 * H, cmulw(cadd(C, D), c->tw + 2 * k));
-      st(x, i0 + 3 * H, cmulw(csub(C, D), c->tw + 2 * (3 * k)));
+static void fft_fwd(const orc_ctx* c, double* x /* interleaved M */) {
+  const uint32_t M = c->M;
+  for (uint32_t s = 0; s < c->logM; ++s) {
+    const uint32_t half = M >> (s + 1);
+    const int sib = c->logM == 10 && (s == 4 || s == 5 || s == 7 || s == 9);
+    for (uint32_t b = 0; b < (1u << s); ++b) {
+      const int mi = sib && (b & 1u);
+      const double* w = c->fwd_lf + 2 * ((1u << s) - 1 + (mi ? b - 1 : b));
+      for (uint32_t j = 0; j < half; ++j) {
+        if (mi)
+          ct_lf_mi(x, 2 * half * b + j, 2 * half * b + j + half, w);
+        else
+          ct_lf(x, 2 * half * b + j, 2 * half * b + j + half, w);
+      }
     }
-}
-
-static void fft_dif(const orc_ctx* c, double* x /* interleaved M */) {
-  if (c->logM != 10) { /* other sizes (toy parameter sets): plain radix-2 */
-    for (uint32_t s = 0; s < c->logM; ++s) r2_dif(c, x, s);
-    return;
   }
-  r4_dif(c, x, 0);
-  r2_dif(c, x, 2);
-  r4_dif(c, x, 3);
-  r2_dif(c, x, 5);
-  r4_dif(c, x, 6);
-  r4_dif(c, x, 8); /* k = 0: every twiddle is W^0 */
 }
 
-static void r2_dit(const orc_ctx* c, double* x, uint32_t s) {
-  const uint32_t M = c->M, half = M >> (s + 1);
-  for (uint32_t blk = 0; blk < M; blk += 2 * half)
-    for (uint32_t j = 0; j < half; ++j) {
-      const cpx p = ld(x, blk + j);
-      const cpx q = cmulwc(ld(x, blk + j + half), c->tw + 2 * ((size_t)j << s));
-      st(x, blk + j, cadd(p, q));
-      st(x, blk + j + half, csub(p, q));
-    }
-}
-
-/* stages s+1 then s, k = j << s */
-static void r4_dit(const orc_ctx* c, double* x, uint32_t s) {
-  const uint32_t M = c->M, H = M >> (s + 2);
-  for (uint32_t blk = 0; blk < M; blk += 4 * H)
-    for (uint32_t j = 0; j < H; ++j) {
-      const size_t k = (size_t)j << s;
-      const uint32_t i0 = blk + j;
-      const cpx x0 = ld(x, i0);
-      const cpx t1 = cmulwc(ld(x, i0 + H), c->tw + 2 * (2 * k));
-      const cpx t2 = cmulwc(ld(x, i0 + 2 * H), c->tw + 2 * k);
-      const cpx t3 = cmulwc(ld(x, i0 + 3 * H), c->tw + 2 * (3 * k));
-      const cpx A = cadd(x0, t1), B = csub(x0, t1), C = cadd(t2, t3), d = csub(t2, t3);
-      const cpx D = {-d.im, d.re}; /* (t2 - t3) * i */
-      st(x, i0, cadd(A, C));
-      st(x, i0 + 2 * H, csub(A, C));
-      st(x, i0 + H, cadd(B, D));
-      st(x, i0 + 3 * H, csub(B, D));
-    }
-}
-
-static void fft_dit_inverse(const orc_ctx* c, double* x) {
-  if (c->logM != 10) {
-    for (int s = (int)c->logM - 1; s >= 0; --s) r2_dit(c, x, (uint32_t)s);
-    return;
+static void fft_inv(const orc_ctx* c, double* x) {
+  const uint32_t M = c->M;
+  for (int s = (int)c->logM - 1; s >= 0; --s) {
+    const uint32_t half = M >> (s + 1);
+    for (uint32_t blk = 0; blk < M; blk += 2 * half)
+      for (uint32_t j = 0; j < half; ++j) {
+        const uint32_t k = j << s;
+        if (half <= 2) {
+          if (k == 0)
+            ct_one(x, blk + j, blk + j + half);
+          else
+            ct_i(x, blk + j, blk + j + half);
+        } else if (c->logM == 10 && s != 2 && s != 5 && s != 7 && k >= M / 4) {
+          ct_lf_i(x, blk + j, blk + j + half, c->inv_lf + 2 * (k - M / 4));
+        } else {
+          ct_lf(x, blk + j, blk + j + half, c->inv_lf + 2 * k);
+        }
+      }
   }
-  r4_dit(c, x, 8); /* stages 9, 8 (k = 0) */
-  r4_dit(c, x, 6);
-  r2_dit(c, x, 5);
-  r4_dit(c, x, 3);
-  r2_dit(c, x, 2);
-  r4_dit(c, x, 0);
 }
 
 static inline uint64_t f64_to_torus(double y) {
@@ -352,15 +345,15 @@ static inline uint64_t f64_to_torus(double y) {
 static void forward_i64(const orc_ctx* c, const int64_t* a, double* out) {
   const uint32_t M = c->M;
   for (uint32_t j = 0; j < M; ++j) {
-    double re = (double)a[j], im = (double)a[j + M];
-    cmul(re, im, c->twist[2 * j], c->twist[2 * j + 1], &out[2 * j], &out[2 * j + 1]);
+    out[2 * j] = (double)a[j];
+    out[2 * j + 1] = (double)a[j + M];
   }
-  fft_dif(c, out);
+  fft_fwd(c, out);
 }
 
 static void backward_torus(const orc_ctx* c, double* spec /* destroyed */, uint64_t* out) {
   const uint32_t M = c->M;
-  fft_dit_inverse(c, spec);
+  fft_inv(c, spec);
   for (uint32_t j = 0; j < M; ++j) {
     double re, im;
     cmul(spec[2 * j], spec[2 * j + 1], c->untwist[2 * j], c->untwist[2 * j + 1], &re, &im);
@@ -455,11 +448,23 @@ static void build_tables(orc_ctx* c) {
   c->logM = 0;
   while ((1u << c->logM) < M) ++c->logM;
   const long double PI = 3.141592653589793238462643383279502884L;
-  c->tw = (double*)malloc(sizeof(double) * 2 * M);
-  for (uint32_t t = 0; t < M; ++t) {
-    long double ang = 2.0L * PI * (long double)t / (long double)M;
-    c->tw[2 * t] = (double)cosl(ang);
-    c->tw[2 * t + 1] = (double)(-sinl(ang));
+  /* Linzer-Feig twiddles (c, t) = (cos, tan), rounded from long double */
+  c->fwd_lf = (double*)malloc(sizeof(double) * 2 * M);
+  for (uint32_t s = 0; s < c->logM; ++s)
+    for (uint32_t b = 0; b < (1u << s); ++b) {
+      uint32_t r = 0; /* brv_s(b) */
+      for (uint32_t q = 0; q < s; ++q) r |= ((b >> q) & 1u) << (s - 1 - q);
+      const int64_t e = ((int64_t)(M >> (s + 1)) * (1 - 4 * (int64_t)r)) % (int64_t)(2 * N);
+      const long double ang = PI * (long double)(e < 0 ? e + 2 * N : e) / (long double)N;
+      double* w = c->fwd_lf + 2 * ((1u << s) - 1 + b);
+      w[0] = (double)cosl(ang);
+      w[1] = (double)tanl(ang);
+    }
+  c->inv_lf = (double*)malloc(sizeof(double) * M);
+  for (uint32_t k = 0; k < M / 2; ++k) {
+    const long double ang = 2.0L * PI * (long double)k / (long double)M; /* conj(W^k) */
+    c->inv_lf[2 * k] = (double)cosl(ang);
+    c->inv_lf[2 * k + 1] = (double)tanl(ang);
   }
   /* twist zeta^j = exp(i pi j / N), j < M, is DEFINED as the product of a
    * fine table (j mod 128) and a coarse table (j div 128), each rounded from
@@ -631,7 +636,8 @@ void orc_destroy(orc_ctx* c) {
   free(c->bskf_hi);
   free(c->bskf_lo);
   free(c->ksk);
-  free(c->tw);
+  free(c->fwd_lf);
+  free(c->inv_lf);
   free(c->twist);
   free(c->untwist);
   free(c->tw_dd);

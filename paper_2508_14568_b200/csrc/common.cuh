@@ -22,12 +22,9 @@ namespace lvb {
 constexpr uint32_t kN = 2048;          // GLWE polynomial size
 constexpr uint32_t kM = kN / 2;        // complex FFT size (negacyclic fold)
 constexpr uint32_t kLogM = 10;
-// FFT twiddle buffer (fft.cuh): kM radix-2 per-stage entries, then three
-// planes of kM >> (s + 2) entries per radix-4 stage pair s in {0,3,4,6,7}.
-__host__ __device__ constexpr uint32_t r4_base(int s) {
-  return s == 0 ? kM : s == 3 ? kM + 768 : s == 4 ? kM + 864 : s == 6 ? kM + 912 : kM + 924;
-}
-constexpr uint32_t kTwEntries = kM + 930;
+// FFT twiddle buffer (fft.cuh twf / twi): kM forward entries (level s,
+// block b at (1 << s) - 1 + b), then kM/2 inverse entries.
+constexpr uint32_t kTwEntries = kM + kM / 2;
 // Spectrum layout of the blind rotation (fft.cuh L_D): register n of
 // thread t = 32 w + L holds DIF output position spec_pos(t, n), bits
 // (x0,x1,x6) = n, (x2,x3,x4,x5,x7) = L, (x8,x9) = w. The Fourier BSK is

@@ -369,21 +369,24 @@ static void pbs_batch(lv_ctx* c, const lv_ct* in, const uint32_t* luts, size_t c
 
 static void build_tables(lv_ctx* c) {
   const long double PI = 3.141592653589793238462643383279502884L;
-  // W[k] = exp(-2 pi i k / kM), k < kM/2, then the per-stage copies
-  // T_s[y] = W[y << s] concatenated (fft.cuh tws()).
-  std::vector<double2> W(kM), tw(kTwEntries), twist(128);
-  for (uint32_t t = 0; t < kM; ++t) {
-    const long double ang = 2.0L * PI * (long double)t / (long double)kM;
-    W[t] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
-  }
+  // Linzer-Feig twiddles (c, t) = (cos, tan) rounded from long double
+  // (oracle build_tables): forward level s block b at (1 << s) - 1 + b is
+  // zeta^e, e = (kM >> (s+1)) (1 - 4 brv_s(b)) mod 2N, zeta = exp(i pi / N);
+  // inverse conj(W^k) = exp(2 pi i k / kM) at kM + k, k < kM/2.
+  std::vector<double2> tw(kTwEntries), twist(128);
   for (uint32_t s = 0; s < kLogM; ++s)
-    for (uint32_t y = 0; y < (kM >> (s + 1)); ++y) tw[(kM - (kM >> s)) + y] = W[y << s];
-  // radix-4 planes (fft.cuh tw4): plane m of pair s holds W[m (j << s)]
-  for (int s : {0, 3, 4, 6, 7}) {
-    const uint32_t H = kM >> (s + 2);
-    for (uint32_t m = 1; m <= 3; ++m)
-      for (uint32_t j = 0; j < H; ++j) tw[r4_base(s) + (m - 1) * H + j] = W[(m * (j << s)) % kM];
+    for (uint32_t b = 0; b < (1u << s); ++b) {
+      uint32_t r = 0;  // brv_s(b)
+      for (uint32_t q = 0; q < s; ++q) r |= ((b >> q) & 1u) << (s - 1 - q);
+      const int64_t e = ((int64_t)(kM >> (s + 1)) * (1 - 4 * (int64_t)r)) % (int64_t)(2 * kN);
+      const long double ang = PI * (long double)(e < 0 ? e + 2 * kN : e) / (long double)kN;
+      tw[((1u << s) - 1) + b] = make_double2((double)cosl(ang), (double)tanl(ang));
+    }
+  for (uint32_t k = 0; k < kM / 2; ++k) {
+    const long double ang = 2.0L * PI * (long double)k / (long double)kM;
+    tw[kM + k] = make_double2((double)cosl(ang), (double)tanl(ang));
   }
+  set_fwd_consts(tw.data());  // levels 0-2 (entries 0..6) as constant operands
   // twist zeta^j = fine[j & 127] * coarse[j >> 7] (oracle build_tables)
   for (uint32_t j = 0; j < 128; ++j) {
     const long double ang = PI * (long double)j / (long double)kN;

@@ -332,49 +332,36 @@ __device__ __forceinline__ double2 sub2(double2 a, double2 b) {
   return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
 }
 
-// radix-2 DIF (u + v, (u - v) w) and DIT (p + q conj(w), p - q conj(w))
-__device__ __forceinline__ void dif(double2& u, double2& v, double2 w) {
-  const double2 s = add2(u, v), d = sub2(u, v);
-  u = s;
-  v = cmul(d, w);
+// Cooley-Tukey butterfly u +- w v in Linzer-Feig form (oracle ct_lf): the
+// twiddle w = c (1 + i t) is held as (c, t) = (w.x, w.y), six FMAs.
+__device__ __forceinline__ void ct(double2& u, double2& v, double2 w) {
+  const double a = __fma_rn(-w.y, v.y, v.x);
+  const double b = __fma_rn(w.y, v.x, v.y);
+  const double2 U = u;
+  u = make_double2(__fma_rn(w.x, a, U.x), __fma_rn(w.x, b, U.y));
+  v = make_double2(__fma_rn(-w.x, a, U.x), __fma_rn(-w.x, b, U.y));
 }
-__device__ __forceinline__ void dit(double2& p, double2& q, double2 w) {
-  const double2 qw = cmul_conj(q, w);
-  const double2 a = add2(p, qw), b = sub2(p, qw);
-  p = a;
-  q = b;
+// u +- (-i w) v (oracle ct_lf_mi): an odd forward block from its even
+// sibling's twiddle; (-i w) v = c (b - i a).
+__device__ __forceinline__ void ct_mi(double2& u, double2& v, double2 w) {
+  const double a = __fma_rn(-w.y, v.y, v.x);
+  const double b = __fma_rn(w.y, v.x, v.y);
+  const double2 U = u;
+  u = make_double2(__fma_rn(w.x, b, U.x), __fma_rn(-w.x, a, U.y));
+  v = make_double2(__fma_rn(-w.x, b, U.x), __fma_rn(w.x, a, U.y));
 }
-
-// radix-4 DIF on (x0, x1, x2, x3) = positions j + {0, H, 2H, 3H} of stages
-// s, s+1 (oracle r4_dif), w1 = W^k, w2 = W^2k, w3 = W^3k with k = j << s.
-__device__ __forceinline__ void dif4(double2& x0, double2& x1, double2& x2, double2& x3,
-                                     double2 w1, double2 w2, double2 w3) {
-  const double2 A = add2(x0, x2), B = add2(x1, x3), C = sub2(x0, x2), d = sub2(x1, x3);
-  const double2 D = make_double2(d.y, -d.x);  // (x1 - x3) * -i
-  x0 = add2(A, B);
-  x1 = cmul(sub2(A, B), w2);
-  x2 = cmul(add2(C, D), w1);
-  x3 = cmul(sub2(C, D), w3);
+// u +- (i w) v (oracle ct_lf_i): an inverse pair with k >= kM/4 from the
+// twiddle of k - kM/4; (i w) v = c (-b + i a).
+__device__ __forceinline__ void ct_pi(double2& u, double2& v, double2 w) {
+  const double a = __fma_rn(-w.y, v.y, v.x);
+  const double b = __fma_rn(w.y, v.x, v.y);
+  const double2 U = u;
+  u = make_double2(__fma_rn(-w.x, b, U.x), __fma_rn(w.x, a, U.y));
+  v = make_double2(__fma_rn(w.x, b, U.x), __fma_rn(-w.x, a, U.y));
 }
-__device__ __forceinline__ void dif4_1(double2& x0, double2& x1, double2& x2, double2& x3) {  // k = 0
-  const double2 A = add2(x0, x2), B = add2(x1, x3), C = sub2(x0, x2), d = sub2(x1, x3);
-  const double2 D = make_double2(d.y, -d.x);
-  x0 = add2(A, B);
-  x1 = sub2(A, B);
-  x2 = add2(C, D);
-  x3 = sub2(C, D);
-}
-// radix-4 DIT on stages s+1 then s (oracle r4_dit).
-__device__ __forceinline__ void dit4(double2& x0, double2& x1, double2& x2, double2& x3,
-                                     double2 w1, double2 w2, double2 w3) {
-  const double2 t1 = cmul_conj(x1, w2), t2 = cmul_conj(x2, w1), t3 = cmul_conj(x3, w3);
-  const double2 A = add2(x0, t1), B = sub2(x0, t1), C = add2(t2, t3), d = sub2(t2, t3);
-  const double2 D = make_double2(-d.y, d.x);  // (t2 - t3) * i
-  x0 = add2(A, C);
-  x2 = sub2(A, C);
-  x1 = add2(B, D);
-  x3 = sub2(B, D);
-}
+// The inverse's first two stages (9, 8): w = 1 on (x0, x1), (x2, x3), then
+// w = 1 on (x0, x2) and w = i on (x1, x3) — exact additions (oracle ct_one,
+// ct_i).
 __device__ __forceinline__ void dit4_1(double2& x0, double2& x1, double2& x2, double2& x3) {
   const double2 A = add2(x0, x1), B = sub2(x0, x1), C = add2(x2, x3), d = sub2(x2, x3);
   const double2 D = make_double2(-d.y, d.x);
@@ -384,28 +371,28 @@ __device__ __forceinline__ void dit4_1(double2& x0, double2& x1, double2& x2, do
   x3 = sub2(B, D);
 }
 
-// Twiddle tables (one buffer, built by context.cu build_tables):
-//   [0, kM): per-stage radix-2 tables T_s[y] = W[y << s] (W[k] =
-//            exp(-2 pi i k / kM)) concatenated, T_s at kM - (kM >> s);
-//   then per radix-4 pair s: three planes of H = kM >> (s+2) entries,
-//            plane m (1..3) holding W[m (j << s)].
-// Same values as the oracle's W table, laid out so every warp-wide load is
-// contiguous or a broadcast.
-__device__ __forceinline__ double2 tws(const double2* __restrict__ tw, int s, uint32_t y) {
+// Twiddle buffer (context.cu build_tables), Linzer-Feig pairs (c, t):
+//   [0, kM): forward, level s block b at (1 << s) - 1 + b: the negacyclic
+//            root zeta^e, e = (kM >> (s+1)) (1 - 4 brv_s(b)) mod 2N;
+//   [kM, kM + kM/2): inverse, conj(W^k) at kM + k.
+// Levels 0-2 (pass A, blocks fixed by registers) also sit in the constant
+// bank, so those butterflies take their twiddles as constant operands.
+__constant__ double2 c_fwd_a[7];  // defined here: fft.cuh has one includer (kernels.cu)
+__device__ __forceinline__ double2 twf(const double2* __restrict__ tw, int s, uint32_t b) {
 #ifdef LVB_ABL_TW  // timing ablation only
-  return make_double2(0.70710678118654757 + s * 1e-3, 0.70710678118654757 - y * 1e-9);
+  return make_double2(0.70710678118654757 + s * 1e-3, 0.9 - b * 1e-9);
 #endif
-  return __ldg(tw + (kM - (kM >> s)) + y);
+  return __ldg(tw + ((1u << s) - 1) + b);
 }
-__device__ __forceinline__ double2 tw4(const double2* __restrict__ tw, int s, int m, uint32_t j) {
+__device__ __forceinline__ double2 twi(const double2* __restrict__ tw, uint32_t k) {
 #ifdef LVB_ABL_TW
-  return make_double2(0.70710678118654757 + s * 1e-3, 0.70710678118654757 - j * 1e-9 - m);
+  return make_double2(0.70710678118654757, 0.9 - k * 1e-9);
 #endif
-  return __ldg(tw + r4_base(s) + (m - 1) * (kM >> (s + 2)) + j);
+  return __ldg(tw + kM + k);
 }
 
 // Coarse twist factors zeta^(128 k), k < 8 (constant bank).
-__constant__ double2 c_twist_coarse[8];  // defined here: fft.cuh has one includer (kernels.cu)
+__constant__ double2 c_twist_coarse[8];
 
 // zeta^x = fine[x & 127] * coarse[x >> 7] (oracle build_tables defines the
 // twist this way); coarse[0] = 1 is an exact identity and is skipped.
@@ -415,8 +402,11 @@ __device__ __forceinline__ double2 twist_at(const double2* __restrict__ fine, ui
 }
 
 // ---------------------------------------------------------------- forward
-// X[p][r] on entry: twisted inputs at x = t + 128 r (L_A). On exit: the
-// spectrum in L_D (register n of thread t = position spec_pos(t, n)).
+// Negacyclic forward transform (oracle fft_fwd): level s pairs bit x(9-s)
+// of the position, block b = x >> (10 - s). X[p][r] on entry: the folded
+// integer polynomial (d_x, d_{x+kM}) at x = t + 128 r (L_A), no twist. On
+// exit: the spectrum in L_D (register n of thread t = position
+// spec_pos(t, n)).
 // buf: NB exchange buffers (no warp may still be reading them); tm: this
 // warp's TMEM lane-quarter base.
 struct NoHook {
@@ -429,131 +419,192 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
                                             const double2* __restrict__ tw, uint32_t t, uint32_t tm,
                                             Hook hook = Hook(), Bar bar = Bar()) {
   const uint32_t L = t & 31, w = t >> 5;
-  // pass A (L_A): radix-4 (0,1) with j = t + 128 r, radix-2 stage 2 (j = t)
-  {
-    double2 w4[2][3];
+  // pass A (L_A: regs (x7, x8, x9)): levels 0, 1, 2; every block index is
+  // a register index, so the twiddles are constant-bank operands
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+  for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int m = 0; m < 3; ++m) w4[r][m] = tw4(tw, 0, m + 1, t + 128 * r);
+    for (int r = 0; r < 4; ++r) ct(X[p][r], X[p][r + 4], c_fwd_a[0]);
 #pragma unroll
-    for (int p = 0; p < P; ++p)
+  for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
-        dif4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w4[r][0], w4[r][1], w4[r][2]);
-    const double2 w2 = tws(tw, 2, t);
+    for (int r = 0; r < 8; r += (r & 1) ? 3 : 1) ct(X[p][r], X[p][r + 2], c_fwd_a[1 + (r >> 2)]);
 #pragma unroll
-    for (int p = 0; p < P; ++p)
+  for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 8; r += 2) dif(X[p][r], X[p][r + 1], w2);
-  }
-  // L_A -> L_B (cross-warp); pass B: radix-4 (3,4) on (x5, x6) = regs
-  // (r1, r2), j = x mod 32 = 16 x4 + u; radix-2 stage 5 on x4 = r0, j = u
+    for (int r = 0; r < 8; r += 2) ct(X[p][r], X[p][r + 1], c_fwd_a[3 + (r >> 1)]);
+  // L_A -> L_B (cross-warp); pass B (L_B: regs (x4, x5, x6), lanes (x7,
+  // x0..x3), warps (x8, x9)): level 3 on x6, block b3 = x >> 7 = 2 w + L0;
+  // level 4 on x5, block 2 b3 + x6; level 5 on x4, block 4 b3 + (x5, x6)
   const uint32_t u = L >> 1;  // x3..x0
   {
-    double2 w4[2][3];
+    const uint32_t b3 = 2 * w + (L & 1);
+    const double2 w3 = twf(tw, 3, b3), w4 = twf(tw, 4, 2 * b3);  // odd level-4 blocks: -i w4
+    double2 w5[2];  // even level-5 blocks 4 b3 + 2 x6; odd ones -i w5
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int m = 0; m < 3; ++m) w4[r][m] = tw4(tw, 3, m + 1, u + 16 * r);
+    for (int q = 0; q < 2; ++q) w5[q] = twf(tw, 5, 4 * b3 + 2 * q);
     xchg_cta<P, NB>(X, buf, bar, [&](int r) { return t + 128u * r; },
                     [&](int r) { return 16u * r + 128u * (L & 1) + u + 256u * w; });
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
-        dif4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w4[r][0], w4[r][1], w4[r][2]);
-    const double2 w5 = tws(tw, 5, u);
+      for (int r = 0; r < 4; ++r) ct(X[p][r], X[p][r + 4], w3);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      ct(X[p][0], X[p][2], w4);
+      ct(X[p][1], X[p][3], w4);
+      ct_mi(X[p][4], X[p][6], w4);
+      ct_mi(X[p][5], X[p][7], w4);
+    }
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 8; r += 2) dif(X[p][r], X[p][r + 1], w5);
+      for (int r = 0; r < 8; r += 4) {
+        ct(X[p][r], X[p][r + 1], w5[r >> 2]);
+        ct_mi(X[p][r + 2], X[p][r + 3], w5[r >> 2]);
+      }
   }
-  // L_B -> L_C (TMEM); pass C: radix-4 (6,7) on (x2, x3) = regs (n0, n1),
-  // j = x mod 4 = (x0, x1) = lanes (3, 4)
+  // L_B -> L_C (TMEM); pass C (L_C: regs (x2, x3, x6), lanes (x4, x5, x7,
+  // x0, x1)): level 6 on x3, block x >> 4 = 16 w + 8 L2 + 4 x6 + 2 L1 + L0;
+  // level 7 on x2, block 2 (x >> 4) + x3
   {
-    const uint32_t j = L >> 3;
-    const double2 w1 = tw4(tw, 6, 1, j), w2 = tw4(tw, 6, 2, j), w3 = tw4(tw, 6, 3, j);
+    const uint32_t b6 = 16 * w + 8 * ((L >> 2) & 1) + 2 * ((L >> 1) & 1) + (L & 1);
+    double2 w6[2], w7[2];  // per x6; odd level-7 blocks (x3 = 1): -i w7
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      w6[q] = twf(tw, 6, b6 + 4 * q);
+      w7[q] = twf(tw, 7, 2 * (b6 + 4 * q));
+    }
     tm_trip_fwd<P>(X, tm);
     hook();
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int n = 0; n < 8; n += 4) dif4(X[p][n], X[p][n + 1], X[p][n + 2], X[p][n + 3], w1, w2, w3);
+      for (int n = 0; n < 8; n += (n & 1) ? 3 : 1) ct(X[p][n], X[p][n + 2], w6[n >> 2]);
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int n = 0; n < 8; n += 4) {
+        ct(X[p][n], X[p][n + 1], w7[n >> 2]);
+        ct_mi(X[p][n + 2], X[p][n + 3], w7[n >> 2]);
+      }
   }
-  // L_C -> L_D (TMEM); pass D: radix-4 (8,9) on (x0, x1) = regs (n0, n1), k = 0
-  tm_trip_fwd<P>(X, tm);
+  // L_C -> L_D (TMEM); pass D (L_D: regs (x0, x1, x6), lanes (x2, x3, x4,
+  // x5, x7)): level 8 on x1, block x >> 2 = 64 w + 32 L4 + 16 x6 + (L & 15);
+  // level 9 on x0, block 2 (x >> 2) + x1
+  {
+    const uint32_t b8 = 64 * w + 32 * (L >> 4) + (L & 15);
+    double2 w8[2], w9[2];  // per x6; odd level-9 blocks (x1 = 1): -i w9
 #pragma unroll
-  for (int p = 0; p < P; ++p)
+    for (int q = 0; q < 2; ++q) {
+      w8[q] = twf(tw, 8, b8 + 16 * q);
+      w9[q] = twf(tw, 9, 2 * (b8 + 16 * q));
+    }
+    tm_trip_fwd<P>(X, tm);
 #pragma unroll
-    for (int n = 0; n < 8; n += 4) dif4_1(X[p][n], X[p][n + 1], X[p][n + 2], X[p][n + 3]);
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int n = 0; n < 8; n += (n & 1) ? 3 : 1) ct(X[p][n], X[p][n + 2], w8[n >> 2]);
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int n = 0; n < 8; n += 4) {
+        ct(X[p][n], X[p][n + 1], w9[n >> 2]);
+        ct_mi(X[p][n + 2], X[p][n + 3], w9[n >> 2]);
+      }
+  }
 }
 
 // ------------------------------------------------------------- inverse
-// X[p][r] on entry: the spectrum in L_D. On exit: L_A (x = t + 128 r), the
-// layout fft_forward's input uses, so each thread owns the same
-// accumulator coefficients in both halves of a CMUX. The cross-warp
-// exchange starts with a CTA barrier (other warps may still read buf).
+// Cyclic DIT inverse (oracle fft_inv): stage s pairs bit x(9-s), j = x mod
+// 2^(9-s), twiddle conj(W^(j << s)). X[p][r] on entry: the spectrum in
+// L_D. On exit: L_A (x = t + 128 r), the layout fft_forward's input uses,
+// so each thread owns the same accumulator coefficients in both halves of
+// a CMUX. The cross-warp exchange starts with a CTA barrier (other warps
+// may still read buf). The untwist is the caller's.
 template <int P, int NB = kXchgBufs, typename Bar = CtaBar>
 __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
                                               const double2* __restrict__ tw, uint32_t t,
                                               uint32_t tm, Bar bar = Bar()) {
   const uint32_t L = t & 31, w = t >> 5;
-  // pass D': radix-4 (9,8) on (x0, x1) = regs (n0, n1), k = 0
+  // pass D': stages 9, 8 on (x0, x1) = regs (n0, n1): w in {1, i}
 #pragma unroll
   for (int p = 0; p < P; ++p)
 #pragma unroll
     for (int n = 0; n < 8; n += 4) dit4_1(X[p][n], X[p][n + 1], X[p][n + 2], X[p][n + 3]);
-  // L_D -> L_C (TMEM); pass C': radix-4 (7,6) on (x2, x3), j = lanes (3, 4)
+  // L_D -> L_C (TMEM); pass C': stage 7 on x2 = n0 (j = (x0, x1) = L >> 3),
+  // stage 6 on x3 = n1 (j = (L >> 3) + 4 x2)
   {
     const uint32_t j = L >> 3;
-    const double2 w1 = tw4(tw, 6, 1, j), w2 = tw4(tw, 6, 2, j), w3 = tw4(tw, 6, 3, j);
+    const double2 v7 = twi(tw, j << 7), v6 = twi(tw, j << 6);  // stage 6, x2 = 1: i v6
     tm_trip_inv<P>(X, tm);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int n = 0; n < 8; n += 4) dit4(X[p][n], X[p][n + 1], X[p][n + 2], X[p][n + 3], w1, w2, w3);
+      for (int n = 0; n < 8; n += 2) ct(X[p][n], X[p][n + 1], v7);
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int n = 0; n < 8; n += 4) {
+        ct(X[p][n], X[p][n + 2], v6);
+        ct_pi(X[p][n + 1], X[p][n + 3], v6);
+      }
   }
-  // L_C -> L_B (TMEM); pass B': radix-2 stage 5 on x4 = r0 (j = u), then
-  // radix-4 (4,3) on (x5, x6) = (r1, r2), j = u + 16 x4
+  // L_C -> L_B (TMEM); pass B': stage 5 on x4 = r0 (j = u), stage 4 on
+  // x5 = r1 (j = u + 16 x4), stage 3 on x6 = r2 (j = u + 16 (x4, x5))
   const uint32_t u = L >> 1;
-  double2 w4[2][3];
   {
-    const double2 w5 = tws(tw, 5, u);
+    const double2 v5 = twi(tw, u << 5), v4 = twi(tw, u << 4);  // stage 4, x4 = 1: i v4
+    double2 v3[2];  // stage 3 per x4; x5 = 1: i v3
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int m = 0; m < 3; ++m) w4[r][m] = tw4(tw, 3, m + 1, u + 16 * r);
+    for (int q = 0; q < 2; ++q) v3[q] = twi(tw, (u << 3) + 128 * q);
     tm_trip_inv<P>(X, tm);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w5);
+      for (int r = 0; r < 8; r += 2) ct(X[p][r], X[p][r + 1], v5);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
-        dit4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w4[r][0], w4[r][1], w4[r][2]);
+      for (int r = 0; r < 8; r += 4) {
+        ct(X[p][r], X[p][r + 2], v4);
+        ct_pi(X[p][r + 1], X[p][r + 3], v4);
+      }
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        ct(X[p][r], X[p][r + 4], v3[r]);
+        ct_pi(X[p][r + 2], X[p][r + 6], v3[r]);
+      }
   }
-  // L_B -> L_A (cross-warp); pass A': radix-2 stage 2 on x7 = r0 (j = t),
-  // radix-4 (1,0) on (x8, x9) = (r1, r2), j = t + 128 r0
-  const double2 w2 = tws(tw, 2, t);
+  // L_B -> L_A (cross-warp); pass A': stage 2 on x7 = r0 (j = t), stage 1
+  // on x8 = r1 (j = t + 128 x7), stage 0 on x9 = r2 (j = t + 128 (x7, x8))
+  const double2 v2 = twi(tw, t << 2), v1 = twi(tw, t << 1);  // stage 1, x7 = 1: i v1
+  double2 v0[2];  // stage 0 per x7; x8 = 1: i v0
 #pragma unroll
-  for (int r = 0; r < 2; ++r)
-#pragma unroll
-    for (int m = 0; m < 3; ++m) w4[r][m] = tw4(tw, 0, m + 1, t + 128 * r);
+  for (int q = 0; q < 2; ++q) v0[q] = twi(tw, t + 128 * q);
   bar.sync();
   xchg_cta<P, NB>(X, buf, bar, [&](int r) { return 16u * r + 128u * (L & 1) + u + 256u * w; },
                   [&](int r) { return t + 128u * r; });
 #pragma unroll
   for (int p = 0; p < P; ++p)
 #pragma unroll
-    for (int r = 0; r < 8; r += 2) dit(X[p][r], X[p][r + 1], w2);
+    for (int r = 0; r < 8; r += 2) ct(X[p][r], X[p][r + 1], v2);
 #pragma unroll
   for (int p = 0; p < P; ++p)
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
-      dit4(X[p][r], X[p][r + 2], X[p][r + 4], X[p][r + 6], w4[r][0], w4[r][1], w4[r][2]);
+    for (int r = 0; r < 8; r += 4) {
+      ct(X[p][r], X[p][r + 2], v1);
+      ct_pi(X[p][r + 1], X[p][r + 3], v1);
+    }
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      ct(X[p][r], X[p][r + 4], v0[r]);
+      ct_pi(X[p][r + 2], X[p][r + 6], v0[r]);
+    }
 }
 
 // f64 -> Z_{2^64}, identical to oracle f64_to_torus. (An integer-pipe

@@ -22,6 +22,9 @@ namespace lvb {
 void set_twist_coarse(const double2* host8) {
   cudaMemcpyToSymbol(c_twist_coarse, host8, 8 * sizeof(double2));
 }
+void set_fwd_consts(const double2* host7) {
+  cudaMemcpyToSymbol(c_fwd_a, host7, 7 * sizeof(double2));
+}
 
 #ifndef LVB_BSK_EVICT_LAST
 #define LVB_BSK_EVICT_LAST 1
@@ -121,7 +124,7 @@ __device__ __forceinline__ double2 mac2(double2 d0, double2 b0, double2 d1, doub
 // evict-last policy: 1 / 2 / 3 / 4 / 5 / 6 / 7 / 8 groups 68.82 / 68.61 /
 // 68.33 / 68.22 / 67.92 / 68.43 / 67.94 / 67.95 ms.
 #ifndef LVB_BSK_EARLY
-#define LVB_BSK_EARLY 8
+#define LVB_BSK_EARLY 4
 #endif
 #ifndef LVB_BSK_EARLY_EXACT
 #define LVB_BSK_EARLY_EXACT 6  // exact-mask kernel (6 values per group): 2 / 3 / 4 / 5 / 6 / 8 groups 93.3 / 92.6 / 89.9 / 90.0 / 89.6 / 89.7 ms
@@ -208,8 +211,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
           const uint64_t rv = s < kN ? pv : (uint64_t)0 - pv;
           d[hpart] = decomp23(rv - own[p][2 * r + hpart]);
         }
-        const double2 tz = TWIST_R(r);
-        X[p][r] = cmul(make_double2((double)d[0], (double)d[1]), tz);
+        X[p][r] = make_double2((double)d[0], (double)d[1]);  // the forward transform twists
       }
     }
 
@@ -316,7 +318,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
   tmem_free(tmem, kTmemCols);
 }
 #ifndef LVB_BR_CTAS
-#define LVB_BR_CTAS 2  // resident CTAs per SM the register allocation targets
+#define LVB_BR_CTAS 3  // resident CTAs per SM the register allocation targets
 #endif
 __global__ void __launch_bounds__(128, LVB_BR_CTAS) blind_rotate_kernel(BrArgs a) {
   blind_rotate_body<false>(a);
@@ -441,7 +443,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
         const uint64_t rv = s < kN ? pv : (uint64_t)0 - pv;
         d[hpart] = decomp23(rv - own[2 * r + hpart]);
       }
-      X[0][r] = cmul(make_double2((double)d[0], (double)d[1]), tz[r]);
+      X[0][r] = make_double2((double)d[0], (double)d[1]);
     }
     fft_forward<1, 1>(X, buf, tw, t, tm);
     const uint32_t my_full = (uint32_t)__cvta_generic_to_shared(&inbox_full[parity]);
@@ -921,7 +923,7 @@ fft_forward_debug_kernel(const int64_t* poly, const double2* __restrict__ tw,
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const uint32_t x = t + 128 * q;
-    X[0][q] = cmul(make_double2((double)poly[x], (double)poly[x + kM]), twist_at(twist, x));
+    X[0][q] = make_double2((double)poly[x], (double)poly[x + kM]);
   }
   fft_forward<1, 1>(X, buf, tw, t, tmem_warp_base(tmem));
 #pragma unroll

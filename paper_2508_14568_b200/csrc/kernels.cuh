@@ -133,6 +133,7 @@ __global__ void fp64_peak_kernel(double* out, int iters, double seed);
 __global__ void flush_kernel(uint4* buf, size_t n16);
 
 void set_twist_coarse(const double2* host8);
+void set_fwd_consts(const double2* host7);
 
 constexpr int kKsItems = 32;
 

@@ -110,8 +110,9 @@ int main() {
     // client / server split: the server evaluates with exported keys only
     GpuBackend client(4000.0, 7);
     const GpuBackend::EvalKeys keys = client.export_keys();
-    CHECK(keys.key_id == 7);
+    CHECK(keys.key_id != 7 && keys.key_id != 0);  // a public-key fingerprint, never the seed
     std::unique_ptr<GpuBackend> server = GpuBackend::evaluation(keys);
+    CHECK(server->key_id() == keys.key_id);
     CHECK(throws<InvalidParams>([&] { server->encrypt(1); }));
     const std::vector<Ct> xs = client.encrypt(std::vector<int32_t>{3, 12, 20});
     std::vector<uint64_t> rows(xs.size() * 2049), back(xs.size() * 2049);
