@@ -129,6 +129,44 @@ __device__ __forceinline__ double2 mac2(double2 d0, double2 b0, double2 d1, doub
 #ifndef LVB_BSK_EARLY_EXACT
 #define LVB_BSK_EARLY_EXACT 6  // exact-mask kernel (6 values per group): 2 / 3 / 4 / 5 / 6 / 8 groups 93.3 / 92.6 / 89.9 / 90.0 / 89.6 / 89.7 ms
 #endif
+// LVB_OWN_TMEM: the thread's owned accumulator coefficients (32 u64) wait
+// out the FFTs in tensor memory (tcgen05.st after the decomposition,
+// tcgen05.ld before the update) instead of being re-read from shared
+// memory, taking 32 KB per CTA and CMUX off the L1/shared data path.
+#ifndef LVB_OWN_TMEM
+#define LVB_OWN_TMEM 1
+#endif
+__device__ __forceinline__ void own_st(uint32_t a, const uint64_t (&o)[2][16]) {
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // 8 u64 = 16 columns per instruction
+      uint32_t r[16];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        r[2 * k] = (uint32_t)o[p][8 * h + k];
+        r[2 * k + 1] = (uint32_t)(o[p][8 * h + k] >> 32);
+      }
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15,%16};" ::"r"(a + 32 * p + 16 * h),
+          "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+          "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+          : "memory");
+    }
+}
+// own[p][8h .. 8h+7] (16 columns); the caller waits (tcgen05.wait::ld).
+__device__ __forceinline__ void own_ld(uint32_t a, int p, int h, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(a + 32 * p + 16 * h)
+      : "memory");
+}
+
 template <bool kExact>
 __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
   constexpr int kEarly = kExact ? LVB_BSK_EARLY_EXACT : LVB_BSK_EARLY;
@@ -137,7 +175,9 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
   double2* buf = reinterpret_cast<double2*>(smem + 2 * kN * 8);        // [kXchgBufs][kM]
   uint16_t* ms = reinterpret_cast<uint16_t*>(smem + 2 * kN * 8 + kXchgBufs * kM * 16);
   __shared__ uint32_t tmem_slot;
-  constexpr uint32_t kTmemCols = kExact ? 128 : 64;  // P spectra x 32 columns (power of 2)
+  // TMEM columns: P spectra x 32 (exchange trips); the throughput kernel also
+  // parks its owned accumulator coefficients at [64, 128) (LVB_OWN_TMEM)
+  constexpr uint32_t kTmemCols = kExact ? 128 : (LVB_OWN_TMEM ? 128 : 64);
   const uint32_t tmem = tmem_alloc(&tmem_slot, kTmemCols);
   const uint32_t tm = tmem_warp_base(tmem);
   const uint32_t t = threadIdx.x;
@@ -214,6 +254,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         X[p][r] = make_double2((double)d[0], (double)d[1]);  // the forward transform twists
       }
     }
+    if constexpr (!kExact && LVB_OWN_TMEM) own_st(tm + 64, own);
 
 #if LVB_BSK_EARLY
     // the first bins' BSK values are requested before the transform's last
@@ -284,6 +325,34 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         X[1][q] = mac2(d1, b11, d0, b01);  // output o: row o first
       }
       fft_inverse_a<2>(X, buf, tw, t, tm);
+#if LVB_OWN_TMEM
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // r in [4h, 4h + 4): own[p][8h .. 8h + 7]
+        uint32_t o0[16], o1[16];
+        own_ld(tm + 64, 0, h, o0);
+        own_ld(tm + 64, 1, h, o1);
+        LVB_TM_WAIT_LD16(o0, o1);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          own[0][8 * h + k] = ((uint64_t)o0[2 * k + 1] << 32) | o0[2 * k];
+          own[1][8 * h + k] = ((uint64_t)o1[2 * k + 1] << 32) | o1[2 * k];
+        }
+#pragma unroll
+        for (int r = 4 * h; r < 4 * h + 4; ++r) {
+          const double2 tv = TWIST_R(r);
+          const double2 ut = make_double2(tv.x, -tv.y);
+          const uint32_t x = t + 128 * r;
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            const double2 z = cmul(X[p][r], ut);
+            own[p][2 * r] += f64_to_torus(z.x);
+            own[p][2 * r + 1] += f64_to_torus(z.y);
+            acc[p * kN + x] = own[p][2 * r];
+            acc[p * kN + x + kM] = own[p][2 * r + 1];
+          }
+        }
+      }
+#else
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const double2 tv = TWIST_R(r);
@@ -300,6 +369,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
           acc[p * kN + x + kM] = own[p][2 * r + 1];
         }
       }
+#endif
     }
   }
 #undef BSK_AT
