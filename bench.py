@@ -387,6 +387,23 @@ def main():
     assert list(ctx.decrypt(out)) == vals, "cfg2 decrypts wrong"
     noise = phase_noise(ctx, out, vals)
     ctx.release(out)
+    # the reference's algorithm on the same keys/encryptions:
+    # its BSK spectrum in plain f64; the measured denominator of the north
+    # star's noise criterion
+    try:
+        pr = L.default_params()
+        pr.exact_mask_product = 2
+        cr = L.Context(seed=0, params=pr, device=local)
+        hr = cr.encrypt(vals)
+        outr = cr.pbs(hr, cr.lut(L.identity_lut()))
+        nref = phase_noise(cr, outr, vals)
+        cr.close()
+        noise["reference_alg_var_log2"] = nref["measured_var_log2"]
+        noise["reference_alg_ratio_to_exact"] = nref["ratio_to_exact"]
+        noise["ratio_to_reference_alg"] = 2.0 ** (noise["measured_var_log2"] -
+                                                   nref["measured_var_log2"])
+    except Exception as e:  # reported, never dropped
+        noise["reference_alg_error"] = repr(e)
 
     ctx.bench_pbs(h, ids, max(3, args.warmup), L2_FLUSH)
     barrier_sync(dist)
@@ -453,9 +470,10 @@ def main():
                                              "blind_rotate_kernel"],
                                 "l2_flush_between_steps": args.steps},
         "clocks": clocks,
-        "phase_noise": dict(noise, note="output phase error of the 4096 cfg2 PBS; FFT-added "
-                            "share predicted 0.19 (dd BSK spectrum), 0.31 for the reference's "
-                            "f64-spectrum algorithm (DESIGN §2)"),
+        "phase_noise": dict(noise, note="output phase error of the 4096 cfg2 PBS vs the exact-"
+                            "product model, and vs the same 4096 PBS with the reference's "
+                            "algorithm (f64 BSK spectrum, exact_mask_product=2) on the same "
+                            "keys and encryptions, measured in this run (DESIGN \u00a72)"),
     }
     if rank == 0 and ws == 1 and not args.no_extras:  # extras and CPU baseline at N=1 only
         try:
@@ -498,6 +516,9 @@ def main():
             ok = list(cx.decrypt(ox)) == vals
             nx = phase_noise(cx, ox, vals)
             bx, _, sx = cx.bench_pbs(hx, np.full(BATCH, lx, np.uint32), max(3, args.steps), L2_FLUSH)
+            if "reference_alg_var_log2" in noise:
+                nx["ratio_to_reference_alg"] = 2.0 ** (nx["measured_var_log2"] -
+                                                       noise["reference_alg_var_log2"])
             line["exact_mask_product"] = {"value": BATCH / (float(np.mean(sx)) / 1e3),
                                           "unit": "PBS/s", "blind_rotate_ms": float(np.mean(bx)),
                                           "correct": ok, "phase_noise": nx,

@@ -62,7 +62,11 @@ typedef struct {
                                 * H 2^43 + Lo with an exactly rounded H product, so
                                 * the FFT adds no key-amplified noise (phase-noise
                                 * variance within 1.001x of exact integer products;
-                                * 1.4x blind-rotation time). DESIGN.md §2. */
+                                * 1.4x blind-rotation time). DESIGN.md §2.
+                                * 2: noise measurement only — the reference's
+                                * algorithm (TFHE-rs f64-FFT PBS): the BSK spectrum
+                                * is the plain f64 transform of the rounded torus
+                                * coefficients instead of our double-double one. */
   int32_t device;              /* CUDA device of the context; -1 (default): the
                                 * calling thread's current device */
 } lv_params;
@@ -216,6 +220,13 @@ int lv_edit_distance_pre_batch(lv_ctx* ctx, size_t npairs, const lv_eqtable* con
                                const char* plains, const uint64_t* plain_off,
                                const lv_band* bands, int32_t key_encoding, lv_ct* scores,
                                lv_run* runs);
+
+/* kernel::distance with a caller-supplied Eq9Provider (kernel.hpp:162-199):
+ * eq9[(i-1) n + (j-1)] is the encrypted scaled equality bit of cell (i, j);
+ * only the in-band cells' handles are read (and must be valid); they stay
+ * owned by the caller. */
+int lv_edit_distance_eq9(lv_ctx* ctx, const lv_ct* eq9, uint64_t m, uint64_t n,
+                         const lv_band* band, int32_t key_encoding, lv_ct* score, lv_run* run);
 
 /* Symbolic schedule of a traversal (no device work): per visited cell
  * (i, j, key variance, refreshes before it) — the observer hook of

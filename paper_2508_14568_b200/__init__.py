@@ -119,7 +119,7 @@ EXPORTS = [
     "lv_get_stats", "lv_get_params", "lv_release", "lv_ledger_variance", "lv_export",
     "lv_import", "lv_phase", "lv_pbs_batch_host", "lv_band_resolve", "lv_edit_distance_ee",
     "lv_edit_distance_batch", "lv_eq_table_build", "lv_eq_table_lookup", "lv_eq_table_destroy",
-    "lv_edit_distance_pre", "lv_edit_distance_pre_batch", "lv_plan_trace", "lv_debug_keys",
+    "lv_edit_distance_pre", "lv_edit_distance_pre_batch", "lv_edit_distance_eq9", "lv_plan_trace", "lv_debug_keys",
     "lv_debug_keyswitch",
     "lv_eq_table_serialize", "lv_eq_table_deserialize",
     "lv_debug_blind_rotate", "lv_debug_fft", "lv_bench_pbs", "lv_bench_fp64_peak",
@@ -189,6 +189,8 @@ def lib():
                                                        ctypes.c_void_p, u64, P(u64)]),
             "lv_edit_distance_pre": (ctypes.c_int, [vp, vp, ctypes.c_char_p, sz, P(Band), i32,
                                                     P(u32), P(Run)]),
+            "lv_edit_distance_eq9": (ctypes.c_int, [vp, P(u32), u64, u64, P(Band), i32, P(u32),
+                                                    P(Run)]),
             "lv_edit_distance_pre_batch": (ctypes.c_int, [vp, sz, P(vp), ctypes.c_char_p, P(u64),
                                                           P(Band), i32, P(u32), P(Run)]),
             "lv_plan_trace": (ctypes.c_int, [u64, u64, P(Band), i32, ctypes.c_double, u64, P(u32),

@@ -188,10 +188,10 @@ static void launch_keyswitch(lv_ctx* c, const LinDesc* d_desc, uint32_t count, u
 // Keys with exact_mask_product use the exact-mask forms of both.
 void launch_blind_rotate(lv_ctx* c, const BrArgs& ba, uint32_t count) {
   if (!count) return;
-  if (c->p.exact_mask_product && count <= c->br_pair_max)
+  if (c->p.exact_mask_product == 1 && count <= c->br_pair_max)
     blind_rotate_pair_exact_kernel<<<2 * count, 128, blind_rotate_pair_smem_bytes(c->p.n),
                                      c->stream>>>(ba);
-  else if (c->p.exact_mask_product)
+  else if (c->p.exact_mask_product == 1)
     blind_rotate_exact_kernel<<<count, 128, blind_rotate_smem_bytes(c->p.n, true), c->stream>>>(ba);
   else if (count <= c->br_pair_max)
     blind_rotate_pair_kernel<<<2 * count, 128, blind_rotate_pair_smem_bytes(c->p.n), c->stream>>>(ba);
@@ -432,7 +432,7 @@ static void gen_bsk(lv_ctx* c, uint64_t* d_bsk) {
 // The resident Fourier BSK (c->d_bskf) from a standard-domain BSK.
 static void derive_bsk(lv_ctx* c, const uint64_t* d_bsk) {
   const uint32_t n = c->p.n;
-  const bool exact = c->p.exact_mask_product != 0;
+  const bool exact = c->p.exact_mask_product == 1;
   const uint32_t nouts = exact ? 3 : 2;  // spectra per GGSW row: [mask, body] or [H, Lo, body]
   LV_CUDA(cudaMalloc(&c->d_bskf, (size_t)n * 8 * kRows * nouts * 128 * sizeof(double2)));
   // double-double twiddle / twist tables for the BSK transform (oracle
@@ -462,8 +462,11 @@ static void derive_bsk(lv_ctx* c, const uint64_t* d_bsk) {
     bsk_split_kernel<<<n * kRows, 256, 0, c->stream>>>(d_bsk, d_split.p);
     LV_CUDA(cudaGetLastError());
   }
-  bsk_fourier_kernel<<<n * kRows * nouts, 512, 0, c->stream>>>(exact ? d_split.p : d_bsk, nouts,
-                                                                d_tw_dd.p, d_twist_dd.p, c->d_bskf);
+  if (c->p.exact_mask_product == 2)  // the reference's algorithm: plain f64 BSK transform
+    bsk_fourier_f64_kernel<<<n * kRows * nouts, 128, 0, c->stream>>>(d_bsk, nouts, c->d_tw, c->d_bskf);
+  else
+    bsk_fourier_kernel<<<n * kRows * nouts, 512, 0, c->stream>>>(exact ? d_split.p : d_bsk, nouts,
+                                                                  d_tw_dd.p, d_twist_dd.p, c->d_bskf);
   LV_CUDA(cudaGetLastError());
   LV_CUDA(cudaStreamSynchronize(c->stream));
 }
@@ -601,8 +604,8 @@ static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bs
     if (p.lwe_noise_log2 < 1 || p.lwe_noise_log2 > 62 || p.glwe_noise_log2 < 1 ||
         p.glwe_noise_log2 > 62)
       throw Error(LV_ERR_INVALID_PARAMS, "noise bounds out of range (TUniform 2^1 .. 2^62)");
-    if (p.exact_mask_product > 1)
-      throw Error(LV_ERR_INVALID_PARAMS, "exact_mask_product must be 0 or 1");
+    if (p.exact_mask_product > 2)
+      throw Error(LV_ERR_INVALID_PARAMS, "exact_mask_product must be 0, 1 or 2");
     if (p.max_variance_budget < 1.0)  // backend.hpp:85-88
       throw Error(LV_ERR_INVALID_PARAMS, "noise budget must be at least 1");
     int ndev = 0;
@@ -644,7 +647,7 @@ static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bs
         if (const char* e = std::getenv("LVB_BR_PAIR_MAX"))
           c->br_pair_max = (uint32_t)std::strtoul(e, nullptr, 10);
         int per_sm = 1;
-        if (p.exact_mask_product)
+        if (p.exact_mask_product == 1)
           LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
               &per_sm, blind_rotate_exact_kernel, 128, blind_rotate_smem_bytes(p.n, true)));
         else
@@ -1030,7 +1033,7 @@ int lv_debug_keys(lv_ctx* c, uint8_t* sk_small, uint8_t* sk_glwe, uint64_t* ksk,
     if (sk_glwe) LV_CUDA(cudaMemcpy(sk_glwe, c->d_sk_glwe, kBig, cudaMemcpyDeviceToHost));
     if (ksk)
       LV_CUDA(cudaMemcpy(ksk, c->d_ksk, (size_t)kBig * kKsLevel * (n + 1) * 8, cudaMemcpyDeviceToHost));
-    if (bskf_nat && c->p.exact_mask_product)
+    if (bskf_nat && c->p.exact_mask_product == 1)
       throw Error(LV_ERR_INVALID_PARAMS, "debug_keys: exact_mask_product keys use the split layout");
     if (bskf_nat) {
       std::vector<double2> raw((size_t)n * 32 * 128);

@@ -965,6 +965,35 @@ bsk_fourier_kernel(const uint64_t* polys, uint32_t nouts, const double4* __restr
   }
 }
 
+// exact_mask_product = 2 (noise measurement only): the reference's algorithm
+// (TFHE-rs v0.7.2) transforms the BSK in plain f64 — the
+// torus coefficient rounded to a double, then the same f64 forward transform
+// the digits take — instead of our double-double transform rounded once.
+// Same layout and 2^-10 pre-scale as bsk_fourier_kernel.
+__global__ void __launch_bounds__(128)
+bsk_fourier_f64_kernel(const uint64_t* polys, uint32_t nouts, const double2* __restrict__ tw,
+                       double2* bskf) {
+  __shared__ double2 buf[kM];
+  __shared__ uint32_t tmem_slot;
+  const uint32_t tmem = tmem_alloc(&tmem_slot, 32);
+  const uint32_t t = threadIdx.x;
+  const uint32_t o = blockIdx.x % nouts, rowi = blockIdx.x / nouts;
+  const uint32_t i = rowi / kRows, r = rowi % kRows;
+  const uint64_t* poly = polys + ((uint64_t)rowi * nouts + o) * kN;
+  double2 X[1][8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t x = t + 128 * q;
+    X[0][q] = make_double2((double)(int64_t)poly[x], (double)(int64_t)poly[x + kM]);
+  }
+  fft_forward<1, 1>(X, buf, tw, t, tmem_warp_base(tmem));
+#pragma unroll
+  for (int q = 0; q < 8; ++q)  // register q of thread t = spectrum slot (t << 3) | q
+    bskf[(size_t)i * (8 * kRows * nouts * 128) + (q * kRows * nouts + r * nouts + o) * 128 + t] =
+        make_double2(__dmul_rn(X[0][q].x, 0x1p-10), __dmul_rn(X[0][q].y, 0x1p-10));
+  tmem_free(tmem, 32);
+}
+
 // exact_mask_product keys: per GGSW row, [H, Lo, body] with the mask
 // coefficient b = H 2^43 + Lo, H = round(b / 2^43) (oracle bsk_range).
 __global__ void bsk_split_kernel(const uint64_t* bsk, uint64_t* split) {

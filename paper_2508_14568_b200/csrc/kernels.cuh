@@ -123,6 +123,8 @@ __global__ void keygen_bsk_kernel(uint64_t seed, uint32_t noise_log2, const uint
                                   const uint8_t* sk_glwe, uint64_t* bsk);
 __global__ void bsk_fourier_kernel(const uint64_t* polys, uint32_t nouts, const double4* tw_dd,
                                    const double4* twist_dd, double2* bskf);
+__global__ void bsk_fourier_f64_kernel(const uint64_t* polys, uint32_t nouts, const double2* tw,
+                                       double2* bskf);
 __global__ void bsk_split_kernel(const uint64_t* bsk, uint64_t* split);
 __global__ void fft_forward_debug_kernel(const int64_t* poly, const double2* tw,
                                          const double2* twist, double2* spec);

@@ -95,6 +95,7 @@ struct PairIn {
   const lv_ct* b;  // n * S symbol handles (ee)
   const lv_eqtable* table = nullptr;
   const char* plain = nullptr;
+  const lv_ct* eq9grid = nullptr;  // caller-supplied eq9 handles, row-major m x n (Eq9Provider)
 };
 
 struct Wave {
@@ -263,6 +264,8 @@ static void run_traversals(lv_ctx* c, const std::vector<PairIn>& pairs, uint32_t
         eq9 = eqs[S - 1];
         r.equality_pbs += S;
         linear_ops += 1 + 4 * (S - 1);
+      } else if (in.eq9grid) {
+        eq9 = in.eq9grid[(size_t)(cell.i - 1) * in.n + (cell.j - 1)];
       } else {
         eq9 = in.table->rows.at(in.plain[cell.j - 1])[cell.i - 1];
       }
@@ -680,6 +683,20 @@ int lv_eq_table_deserialize(lv_ctx* c, const uint8_t* buf, uint64_t len, lv_eqta
       throw;
     }
     *out = t;
+  });
+}
+
+int lv_edit_distance_eq9(lv_ctx* c, const lv_ct* eq9, uint64_t m, uint64_t n, const lv_band* band,
+                         int32_t key_encoding, lv_ct* score, lv_run* run) {
+  return guard_wf([&] {
+    CtxLock lk(c);
+    PairIn in{(uint32_t)m, (uint32_t)n, to_band(band), nullptr, nullptr, nullptr, nullptr, eq9};
+    const auto plan = get_plan(c, in.m, in.n, in.band, key_encoding == LV_KEY_NEGATED,
+                               c->p.max_variance_budget);
+    for (const CellPlan& cell : plan->cells)  // only the visited cells' handles are read
+      check_handles(c, eq9 + (size_t)(cell.i - 1) * n + (cell.j - 1), 1);
+    std::vector<PairIn> pairs{in};
+    run_traversals(c, pairs, 0, key_encoding == LV_KEY_NEGATED, score, run);
   });
 }
 

@@ -241,6 +241,23 @@ def distance_encrypted(ctx: Context, a: EncryptedString, b: EncryptedString, ban
     return _run(run, score.value)
 
 
+def distance(ctx: Context, eq9_provider, m: int, n: int, band: BandSpec,
+             encoding: str = "negated") -> DistanceRun:
+    """kernel::distance with an Eq9Provider (kernel.hpp:162-199):
+    eq9_provider(i, j) -> handle of the encrypted 9*[a_i == b_j] for every
+    in-band cell (1-based), asked in the reference's visiting order."""
+    grid = np.zeros(max(m * n, 1), np.uint32)
+    cells, _ = plan_trace(m, n, band, encoding, ctx.params.max_variance_budget)
+    for i, j, _, _ in cells:
+        grid[(i - 1) * n + (j - 1)] = eq9_provider(i, j)
+    score = ctypes.c_uint32()
+    run = Run()
+    bc = band._c()
+    _check(lib().lv_edit_distance_eq9(ctx._h, _ptr(grid, ctypes.c_uint32), m, n, ctypes.byref(bc),
+                                      _key_enc(encoding), ctypes.byref(score), ctypes.byref(run)))
+    return _run(run, score.value)
+
+
 def distance_batch(ctx: Context, pairs, bands, encoding: str = "negated"):
     """All pairs' same-index anti-diagonals share one launch."""
     # symbols per character from the arrays' shape (empty strings keep (0, S));

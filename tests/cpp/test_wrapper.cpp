@@ -1,6 +1,10 @@
 // Reference-shaped C++ tests over include/leuven_b200.hpp, mirroring cases of
 // proj/tests/unit/test_backend.cpp and test_kernel.cpp. Exit code = failures.
 #include <cstdio>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -42,7 +46,119 @@ static EncryptedString enc_ascii(GpuBackend& b, const std::string& s) {
   return e;
 }
 
-int main() {
+// One golden case per line (written by tests/test_gpu_cpp_wrapper.py from
+// tests/golden/reference_runs.json): a, b, mode, ell, encoding, budget,
+// key encoding, preprocess, the reference's report_json — tab-separated.
+static std::vector<std::vector<std::string>> read_cases(const char* path) {
+  std::vector<std::vector<std::string>> out;
+  std::ifstream in(path);
+  std::string line;
+  while (std::getline(in, line)) {
+    std::vector<std::string> f;
+    std::stringstream ss(line);
+    std::string x;
+    while (std::getline(ss, x, '\t')) f.push_back(x);
+    if (f.size() == 9) out.push_back(f);
+  }
+  return out;
+}
+
+static void pipeline_api(const char* cases_path) {
+  using namespace leuven::b200::cli;
+  {  // encoding.hpp builtins (encoding.cpp:78-96, 169-190)
+    CHECK(AlphabetSpec::ascii7().charset().size() == 128);
+    CHECK(AlphabetSpec::lower26().charset().size() == 26);
+    CHECK(AlphabetSpec::dna4().charset().size() == 4);
+    CHECK(AlphabetSpec::ascii7().symbol_count() == 2 && AlphabetSpec::ascii7().bit_width() == 7);
+    CHECK(AlphabetSpec::dna4().code_of('G') == 2);
+    CHECK(throws<CharNotInAlphabet>([] { AlphabetSpec::dna4().code_of('X'); }));
+    CHECK(throws<InvalidParams>([] { AlphabetSpec::builtin("custom:x"); }));
+    for (const AlphabetSpec* a : {&AlphabetSpec::ascii7(), &AlphabetSpec::lower26(), &AlphabetSpec::dna4()})
+      for (char c : a->charset()) CHECK(decode_char(encode_char(c, *a), *a) == c);
+    const EncodedChar e = encode_char('K', AlphabetSpec::ascii7());  // 75 = 0x4B -> (11, 4)
+    CHECK(e.symbols.size() == 2 && e.symbols[0] == 11 && e.symbols[1] == 4);
+  }
+  GpuBackend be(4000.0, 5);
+  {  // encrypt_string / decrypt_string round trip
+    const EncryptedString x = encrypt_string("Hello, B200!", AlphabetSpec::ascii7(), be);
+    CHECK(x.length() == 12 && x.symbols == 2);
+    CHECK(decrypt_string(x, AlphabetSpec::ascii7(), be) == "Hello, B200!");
+    CHECK(throws<CharNotInAlphabet>([&] { encrypt_string("ACGU", AlphabetSpec::dna4(), be); }));
+  }
+  {  // kernel::distance with an Eq9Provider + observer (kernel.hpp:162-199)
+    const std::string a = "KID", b = "SIT";
+    std::vector<Ct> eqs;
+    size_t seen = 0;
+    DistanceOptions opt;
+    opt.observer = [&](const CellObservation& o) {
+      ++seen;
+      CHECK(o.key_variance > 0 && o.i >= 1 && o.j >= 1);
+    };
+    const DistanceRun r = distance(be, [&](size_t i, size_t j) {
+      eqs.push_back(be.encrypt(a[i - 1] == b[j - 1] ? 9 : 0));
+      return eqs.back();
+    }, a.size(), b.size(), BandSpec::exact(3, 3), opt);
+    CHECK(be.decrypt(r.score) == 2);
+    CHECK(seen == 9 && eqs.size() == 9 && r.counters.kernel_pbs == 9 && r.counters.equality_pbs == 0);
+  }
+  {  // distance_batch == per-pair distance_encrypted
+    const std::vector<std::pair<std::string, std::string>> ps = {{"kitten", "sitting"}, {"", "abc"},
+                                                                 {"flaw", "lawn"}};
+    std::vector<std::pair<EncryptedString, EncryptedString>> enc;
+    std::vector<BandSpec> bands;
+    for (const auto& p : ps) {
+      enc.push_back({encrypt_string(p.first, AlphabetSpec::ascii7(), be),
+                     encrypt_string(p.second, AlphabetSpec::ascii7(), be)});
+      bands.push_back(BandSpec::exact(p.first.size(), p.second.size()));
+    }
+    const std::vector<DistanceRun> rs = distance_batch(be, enc, bands);
+    CHECK(rs.size() == 3 && be.decrypt(rs[0].score) == 3 && be.decrypt(rs[1].score) == 3 &&
+          be.decrypt(rs[2].score) == 2);
+    CHECK(rs[0].counters.kernel_pbs == 42 && rs[0].counters.equality_pbs == 84);
+  }
+  {  // cli::compute_report / report_json on the compiled reference's cases
+    const auto cases = read_cases(cases_path);
+    CHECK(cases.size() >= 20);
+    std::vector<std::pair<std::string, std::string>> batch_pairs;
+    std::vector<std::string> batch_want;
+    std::map<double, std::unique_ptr<GpuBackend>> by_budget;
+    for (const auto& f : cases) {
+      ComputeConfig c;
+      c.a = f[0];
+      c.b = f[1];
+      c.mode = f[2];
+      c.has_ell = c.mode == "approx";
+      c.ell = std::stoull(f[3]);
+      c.encoding = f[4];
+      c.budget = std::stod(f[5]);
+      c.key_encoding = f[6];
+      c.preprocess = f[7] == "1";
+      std::unique_ptr<GpuBackend>& b2 = by_budget[c.budget];  // one key set per budget
+      if (!b2) b2.reset(new GpuBackend(c.budget, 9));
+      const RunReport r = compute_report(c, b2.get());
+      const std::string got = report_json(r, false);
+      if (got != f[8]) std::printf("report %s | %s\n  got  %s\n  want %s\n", f[0].c_str(), f[1].c_str(),
+                                   got.c_str(), f[8].c_str());
+      CHECK(got == f[8]);
+      CHECK(report_json(r, true).find("\"wall_time_ms\":") != std::string::npos);
+      if (c.mode == "exact" && c.encoding == "ascii7" && c.budget == 4000.0 && !c.preprocess &&
+          c.key_encoding == "negated") {
+        batch_pairs.push_back({c.a, c.b});
+        batch_want.push_back(f[8]);
+      }
+    }
+    // the same cases through compute_batch: one wavefront, identical reports
+    ComputeConfig base;
+    const std::vector<RunReport> rs = compute_batch(batch_pairs, base, &be);
+    CHECK(rs.size() == batch_pairs.size() && !rs.empty());
+    for (size_t i = 0; i < rs.size(); ++i) CHECK(report_json(rs[i], false) == batch_want[i]);
+    CHECK(human_report(compute_report({"KID", "SIT"}, &be)).rfind("distance: 2\n", 0) == 0);
+    CHECK(classify_error_exit(BandTooNarrow("x")) == 3 && classify_error_exit(InvalidParams("x")) == 2);
+  }
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1) pipeline_api(argv[1]);
   {
     // test_backend.cpp:202-219 (tight budget, Table-1 x-4 LUT)
     GpuBackend b(25.0);

@@ -147,6 +147,33 @@ def test_measured_output_noise_4096(exact_mask):
         ratio = float(np.var(e.astype(np.float64))) / exact_model_var()
         lo, hi = (1.07, 1.32) if exact_mask == 0 else (0.89, 1.11)
         assert lo < ratio < hi, ratio
-        assert ratio < 1.1 * 1.31  # within 1.1x of the reference's algorithm
     finally:
         c.close()
+
+
+def _phase_errors(mode: int, vals):
+    p = L.default_params()
+    p.exact_mask_product = mode
+    c = L.Context(seed=11, params=p)
+    try:
+        out = c.pbs(c.encrypt(vals), L.identity_lut())
+        return (c.phase(out) - np.asarray(vals, np.uint64) * np.uint64(1 << 59)).view(np.int64)
+    finally:
+        c.close()
+
+
+def test_noise_vs_reference_algorithm_measured():
+    """North-star noise criterion against a MEASURED denominator: the same
+    4096 bootstraps (same seed, so the same keys, encryptions and exact-
+    product noise) with the reference's algorithm — exact_mask_product = 2,
+    the TFHE-rs f64-FFT PBS whose BSK spectrum is the plain f64 transform —
+    on this GPU. The shared exact-product noise cancels in the ratio, so
+    4096 samples pin it to about +-1%. Ours (double-double BSK spectrum)
+    and the exact-mask keys must stay within 1.1x of it; measured r02:
+    0.91x and 0.76x."""
+    vals = [(5 * i + 3) % 16 for i in range(4096)]
+    ref = float(np.var(_phase_errors(2, vals).astype(np.float64)))
+    assert 1.15 < ref / exact_model_var() < 1.55, ref / exact_model_var()  # model 1 + 0.31
+    for mode, hi in ((0, 1.0), (1, 0.85)):
+        v = float(np.var(_phase_errors(mode, vals).astype(np.float64)))
+        assert v / ref < hi < 1.1, (mode, v / ref)
