@@ -51,7 +51,7 @@ def test_context_rejects_bad_params(product_lib):
     """Parameter validation happens before any device work (InvalidParams)."""
     for field, value in (("N", 1024), ("k", 2), ("pbs_base_log", 22), ("ks_level", 4), ("n", 0),
                          ("n", 5000), ("lwe_noise_log2", 63), ("glwe_noise_log2", 0),
-                         ("exact_mask_product", 2), ("max_variance_budget", 0.5)):
+                         ("exact_mask_product", 3), ("max_variance_budget", 0.5)):
         p = L.default_params()
         setattr(p, field, value)
         with pytest.raises(L.InvalidParams):
