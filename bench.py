@@ -475,6 +475,22 @@ def main():
                             "algorithm (f64 BSK spectrum, exact_mask_product=2) on the same "
                             "keys and encryptions, measured in this run (DESIGN \u00a72)"),
     }
+    if args.cfg5 and ws > 1:  # cfg5 pairs sharded over the ranks (shard.compute_batch_sharded)
+        from paper_2508_14568_b200 import shard
+        pairs = W.cfg5(256)
+        L.compute_batch(pairs[:2], ctx=ctx)  # warm
+        barrier_sync(dist)
+        t0 = time.perf_counter()
+        reps = shard.compute_batch_sharded(pairs, rank, ws, ctx=ctx)
+        barrier_sync(dist)
+        dt = reduce_max(dist, time.perf_counter() - t0)
+        gold = golden_configs()["cfg5"]
+        cells = sum(r["visited_cells"] for r in reps)
+        line["dp_cells"] = {"cfg5_sharded": {
+            "pairs": len(pairs), "ranks": ws, "cells": cells, "seconds": dt, "cells_per_s": cells / dt,
+            "distances_ok": all(r["distance"] == g["report"]["distance"] for r, g in zip(reps, gold)),
+            "note": "pairs[rank::world] per GPU, one compute_batch wavefront each, reports "
+                    "gathered (all_gather_object); time = max over ranks"}}
     if rank == 0 and ws == 1 and not args.no_extras:  # extras and CPU baseline at N=1 only
         try:
             line["dp_cells"] = dp_cells(ctx, args.cfg5)

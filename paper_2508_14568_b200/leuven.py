@@ -457,29 +457,41 @@ def compute(a: str, b: str, mode: str = "exact", ell=None, encoding: str = "asci
     } | ({"wall_time_ms": (t1 - t0) * 1e3} if include_timing else {})
 
 
-def compute_batch(pairs, encoding: str = "ascii7", budget: float = 4000.0,
-                  key_encoding: str = "negated", ctx: Context | None = None, seed: int | None = None):
-    """Batch mode (cli.cpp:164-210): exact band, one report per pair, all
-    pairs traversed together on the GPU."""
-    spec = AlphabetSpec.by_name(encoding)
-    ctx = ctx if ctx is not None else _context(seed, budget)
+def _traverse_batch(ctx: Context, pairs, spec: AlphabetSpec, bands, key_encoding: str):
+    """The GPU part of compute_batch: encrypt every string, one wavefront over
+    all pairs, decrypt the scores. Returns [(distance, DistanceRun)]."""
     enc = []
     for a, b in pairs:
         enc.append((encrypt_string(a, spec, ctx), encrypt_string(b, spec, ctx)))
-    bands = [BandSpec.exact(len(a), len(b)) for a, b in pairs]
     runs = distance_batch(ctx, enc, bands, key_encoding)
     dists = ctx.decrypt([r.score for r in runs]) if runs else []
-    out = []
-    for r, d in zip(runs, dists):
-        out.append({"distance": int(d), "visited_cells": r.visited_cells,
-                    "pbs_equality": r.equality_pbs, "pbs_kernel": r.kernel_pbs,
-                    "pbs_total": r.equality_pbs + r.kernel_pbs + r.refreshes,
-                    "refresh_count": r.refreshes, "max_key_variance": r.max_key_variance})
     ctx.release([r.score for r in runs])
     for x, y in enc:
         for t in (x.chars, y.chars):
             if t.size:
                 ctx.release(t)
+    return [(int(d), r) for d, r in zip(dists, runs)]
+
+
+def compute_batch(pairs, encoding: str = "ascii7", budget: float = 4000.0,
+                  key_encoding: str = "negated", ctx: Context | None = None, seed: int | None = None,
+                  _traverse=None):
+    """Batch mode (cli.cpp:164-210): exact band, one report per pair, all
+    pairs traversed together on the GPU. (_traverse: the GPU part, replaced
+    only by the CPU multi-process test.)"""
+    spec = AlphabetSpec.by_name(encoding)
+    bands = [BandSpec.exact(len(a), len(b)) for a, b in pairs]
+    if _traverse is None:
+        ctx = ctx if ctx is not None else _context(seed, budget)
+        _traverse = _traverse_batch
+    out = []
+    for (d, r), band in zip(_traverse(ctx, pairs, spec, bands, key_encoding), bands):
+        out.append({"distance": d, "mode": "exact", "half_width": band.half_width,
+                    "visited_cells": r.visited_cells, "pbs_equality": r.equality_pbs,
+                    "pbs_kernel": r.kernel_pbs,
+                    "pbs_total": r.equality_pbs + r.kernel_pbs + r.refreshes,
+                    "refresh_count": r.refreshes, "preprocessing_pbs": 0,
+                    "max_key_variance": r.max_key_variance})
     return out
 
 

@@ -37,3 +37,14 @@ def run_sharded(items, fn, rank: int, world: int):
     mine = shard(items, rank, world)
     res = fn([it for _, it in mine]) if mine else []
     return gather_results(list(zip([i for i, _ in mine], res)), world, len(items))
+
+
+def compute_batch_sharded(pairs, rank: int, world: int, ctx=None, _traverse=None, **kw):
+    """cfg5-style batch across ranks: this rank runs compute_batch (one
+    wavefront on its own GPU and key replica) over pairs[rank::world];
+    every rank returns all reports in input order (gathered as plain dicts,
+    never ciphertexts). The reference's own concurrency is one thread per
+    pair (cli.cpp:194-207); here each rank's shard is one launch sequence."""
+    from . import leuven
+    return run_sharded(pairs, lambda ps: leuven.compute_batch(ps, ctx=ctx, _traverse=_traverse, **kw),
+                       rank, world)
