@@ -13,6 +13,9 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_build", "liboracle.so")
+# the same source built -O3 for x86-64-v3 (AVX2 + hardware FMA): the CPU
+# baseline's fast build; bit-identical outputs (explicit fma(), no contraction)
+FAST_LIB_PATH = os.path.join(HERE, "_build", "liboracle_fast.so")
 
 
 class Params(ctypes.Structure):
@@ -38,15 +41,15 @@ def build():
     subprocess.run(["make", "-s", "-C", HERE, "all"], check=True)
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        if not os.path.exists(LIB_PATH):
+def lib(fast: bool = False):
+    if fast not in _libs:
+        path = FAST_LIB_PATH if fast else LIB_PATH
+        if not os.path.exists(path):
             build()
-        L = ctypes.CDLL(LIB_PATH)
+        L = ctypes.CDLL(path)
         u64p = ctypes.POINTER(ctypes.c_uint64)
         i32p = ctypes.POINTER(ctypes.c_int32)
         u32p = ctypes.POINTER(ctypes.c_uint32)
@@ -89,8 +92,8 @@ def lib():
         L.orc_pbs_batch.argtypes = [vp, ctypes.c_size_t, u64p, i32p, u64p, ctypes.c_int, ctypes.c_int]
         L.orc_fft_forward_i64.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double)]
         L.orc_fft_backward_torus.argtypes = [vp, ctypes.POINTER(ctypes.c_double), u64p]
-        _lib = L
-    return _lib
+        _libs[fast] = L
+    return _libs[fast]
 
 
 def _p(a, ct):
@@ -112,10 +115,12 @@ def toy_params() -> Params:
 class Oracle:
     """One keyset: all keys derived from `seed` (Philox domains)."""
 
-    def __init__(self, seed: int = 0, params: Params | None = None, threads: int = 0):
+    def __init__(self, seed: int = 0, params: Params | None = None, threads: int = 0,
+                 fast: bool = False):
         self.params = params if params is not None else default_params()
         self.seed = seed
-        self._c = lib().orc_create(ctypes.byref(self.params), seed, threads)
+        self._L = lib(fast)
+        self._c = self._L.orc_create(ctypes.byref(self.params), seed, threads)
         p = self.params
         self.n, self.N, self.k = p.n, p.N, p.k
         self.big = p.k * p.N + 1
@@ -123,78 +128,78 @@ class Oracle:
 
     def __del__(self):
         if getattr(self, "_c", None):
-            lib().orc_destroy(self._c)
+            self._L.orc_destroy(self._c)
             self._c = None
 
     # keys -----------------------------------------------------------
     def sk_small(self):
-        return np.ctypeslib.as_array(lib().orc_sk_small(self._c), (self.n,)).copy()
+        return np.ctypeslib.as_array(self._L.orc_sk_small(self._c), (self.n,)).copy()
 
     def sk_glwe(self):
-        return np.ctypeslib.as_array(lib().orc_sk_glwe(self._c), (self.k * self.N,)).copy()
+        return np.ctypeslib.as_array(self._L.orc_sk_glwe(self._c), (self.k * self.N,)).copy()
 
     def ksk(self):
         p = self.params
-        return np.ctypeslib.as_array(lib().orc_ksk(self._c), (p.k * p.N * p.ks_level * (p.n + 1),)).copy()
+        return np.ctypeslib.as_array(self._L.orc_ksk(self._c), (p.k * p.N * p.ks_level * (p.n + 1),)).copy()
 
     def bsk(self):
-        return np.ctypeslib.as_array(lib().orc_bsk(self._c), (self.n * self.rows * (self.k + 1) * self.N,)).copy()
+        return np.ctypeslib.as_array(self._L.orc_bsk(self._c), (self.n * self.rows * (self.k + 1) * self.N,)).copy()
 
     def bskf(self):
-        return np.ctypeslib.as_array(lib().orc_bskf(self._c), (self.n * self.rows * (self.k + 1) * self.N,)).copy()
+        return np.ctypeslib.as_array(self._L.orc_bskf(self._c), (self.n * self.rows * (self.k + 1) * self.N,)).copy()
 
     def bskf_split(self):
         """(H, Lo) spectra of the mask polynomials (exact_mask_product keys)."""
         size = (self.n * self.rows * self.k * self.N,)
-        return (np.ctypeslib.as_array(lib().orc_bskf_hi(self._c), size).copy(),
-                np.ctypeslib.as_array(lib().orc_bskf_lo(self._c), size).copy())
+        return (np.ctypeslib.as_array(self._L.orc_bskf_hi(self._c), size).copy(),
+                np.ctypeslib.as_array(self._L.orc_bskf_lo(self._c), size).copy())
 
     # ciphertexts ----------------------------------------------------
     def encrypt(self, value: int, counter: int) -> np.ndarray:
         out = np.zeros(self.big, np.uint64)
-        lib().orc_encrypt_at(self._c, int(value), int(counter), _p(out, ctypes.c_uint64))
+        self._L.orc_encrypt_at(self._c, int(value), int(counter), _p(out, ctypes.c_uint64))
         return out
 
     def trivial(self, value: int) -> np.ndarray:
         out = np.zeros(self.big, np.uint64)
-        lib().orc_trivial(self._c, int(value), _p(out, ctypes.c_uint64))
+        self._L.orc_trivial(self._c, int(value), _p(out, ctypes.c_uint64))
         return out
 
     def phase(self, ct: np.ndarray) -> int:
         ct = np.ascontiguousarray(ct, np.uint64)
-        return int(lib().orc_phase(self._c, _p(ct, ctypes.c_uint64)))
+        return int(self._L.orc_phase(self._c, _p(ct, ctypes.c_uint64)))
 
     def decrypt(self, ct: np.ndarray) -> int:
         ct = np.ascontiguousarray(ct, np.uint64)
-        return int(lib().orc_decrypt(self._c, _p(ct, ctypes.c_uint64)))
+        return int(self._L.orc_decrypt(self._c, _p(ct, ctypes.c_uint64)))
 
     def keyswitch(self, ct: np.ndarray) -> np.ndarray:
         ct = np.ascontiguousarray(ct, np.uint64)
         out = np.zeros(self.n + 1, np.uint64)
-        lib().orc_keyswitch(self._c, _p(ct, ctypes.c_uint64), _p(out, ctypes.c_uint64))
+        self._L.orc_keyswitch(self._c, _p(ct, ctypes.c_uint64), _p(out, ctypes.c_uint64))
         return out
 
     def modswitch(self, small: np.ndarray) -> np.ndarray:
         small = np.ascontiguousarray(small, np.uint64)
         out = np.zeros(self.n + 1, np.uint32)
-        lib().orc_modswitch(self._c, _p(small, ctypes.c_uint64), _p(out, ctypes.c_uint32))
+        self._L.orc_modswitch(self._c, _p(small, ctypes.c_uint64), _p(out, ctypes.c_uint32))
         return out
 
     def phase_small(self, small: np.ndarray) -> int:
         small = np.ascontiguousarray(small, np.uint64)
-        return int(lib().orc_phase_small(self._c, _p(small, ctypes.c_uint64)))
+        return int(self._L.orc_phase_small(self._c, _p(small, ctypes.c_uint64)))
 
     def test_poly(self, lut) -> np.ndarray:
         lut = np.ascontiguousarray(lut, np.int32)
         out = np.zeros(self.N, np.uint64)
-        lib().orc_test_poly(self._c, _p(lut, ctypes.c_int32), _p(out, ctypes.c_uint64))
+        self._L.orc_test_poly(self._c, _p(lut, ctypes.c_int32), _p(out, ctypes.c_uint64))
         return out
 
     def blind_rotate(self, ms: np.ndarray, tp: np.ndarray, mode: int = 0) -> np.ndarray:
         ms = np.ascontiguousarray(ms, np.uint32)
         tp = np.ascontiguousarray(tp, np.uint64)
         out = np.zeros((self.k + 1) * self.N, np.uint64)
-        lib().orc_blind_rotate(self._c, _p(ms, ctypes.c_uint32), _p(tp, ctypes.c_uint64),
+        self._L.orc_blind_rotate(self._c, _p(ms, ctypes.c_uint32), _p(tp, ctypes.c_uint64),
                                _p(out, ctypes.c_uint64), mode)
         return out
 
@@ -202,7 +207,7 @@ class Oracle:
         ms = np.ascontiguousarray(ms, np.uint32).reshape(-1, self.n + 1)
         tp = np.ascontiguousarray(tp, np.uint64)
         out = np.zeros((ms.shape[0], (self.k + 1) * self.N), np.uint64)
-        lib().orc_blind_rotate_batch(self._c, ms.shape[0], _p(ms, ctypes.c_uint32),
+        self._L.orc_blind_rotate_batch(self._c, ms.shape[0], _p(ms, ctypes.c_uint32),
                                      _p(tp, ctypes.c_uint64), _p(out, ctypes.c_uint64), mode, threads)
         return out
 
@@ -211,19 +216,19 @@ class Oracle:
         products computed alongside on the same inputs)."""
         ms = np.ascontiguousarray(ms, np.uint32)
         tp = np.ascontiguousarray(tp, np.uint64)
-        return lib().orc_fft_phase_error_var(self._c, _p(ms, ctypes.c_uint32), _p(tp, ctypes.c_uint64))
+        return self._L.orc_fft_phase_error_var(self._c, _p(ms, ctypes.c_uint32), _p(tp, ctypes.c_uint64))
 
     def sample_extract(self, glwe: np.ndarray) -> np.ndarray:
         glwe = np.ascontiguousarray(glwe, np.uint64)
         out = np.zeros(self.big, np.uint64)
-        lib().orc_sample_extract(self._c, _p(glwe, ctypes.c_uint64), _p(out, ctypes.c_uint64))
+        self._L.orc_sample_extract(self._c, _p(glwe, ctypes.c_uint64), _p(out, ctypes.c_uint64))
         return out
 
     def pbs(self, ct: np.ndarray, lut, mode: int = 0) -> np.ndarray:
         ct = np.ascontiguousarray(ct, np.uint64)
         lut = np.ascontiguousarray(lut, np.int32)
         out = np.zeros(self.big, np.uint64)
-        lib().orc_pbs(self._c, _p(ct, ctypes.c_uint64), _p(lut, ctypes.c_int32),
+        self._L.orc_pbs(self._c, _p(ct, ctypes.c_uint64), _p(lut, ctypes.c_int32),
                       _p(out, ctypes.c_uint64), mode)
         return out
 
@@ -232,20 +237,20 @@ class Oracle:
         luts = np.ascontiguousarray(luts, np.int32).reshape(-1, 16)
         assert cts.shape[0] == luts.shape[0]
         out = np.zeros_like(cts)
-        lib().orc_pbs_batch(self._c, cts.shape[0], _p(cts, ctypes.c_uint64),
+        self._L.orc_pbs_batch(self._c, cts.shape[0], _p(cts, ctypes.c_uint64),
                             _p(luts, ctypes.c_int32), _p(out, ctypes.c_uint64), mode, threads)
         return out
 
     def fft_forward(self, poly: np.ndarray) -> np.ndarray:
         poly = np.ascontiguousarray(poly, np.int64)
         out = np.zeros(self.N, np.float64)
-        lib().orc_fft_forward_i64(self._c, _p(poly, ctypes.c_int64), _p(out, ctypes.c_double))
+        self._L.orc_fft_forward_i64(self._c, _p(poly, ctypes.c_int64), _p(out, ctypes.c_double))
         return out
 
     def fft_backward(self, spec: np.ndarray) -> np.ndarray:
         spec = np.ascontiguousarray(spec, np.float64)
         out = np.zeros(self.N, np.uint64)
-        lib().orc_fft_backward_torus(self._c, _p(spec, ctypes.c_double), _p(out, ctypes.c_uint64))
+        self._L.orc_fft_backward_torus(self._c, _p(spec, ctypes.c_double), _p(out, ctypes.c_uint64))
         return out
 
 
