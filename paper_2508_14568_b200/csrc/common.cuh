@@ -22,8 +22,15 @@ namespace lvb {
 constexpr uint32_t kN = 2048;          // GLWE polynomial size
 constexpr uint32_t kM = kN / 2;        // complex FFT size (negacyclic fold)
 constexpr uint32_t kLogM = 10;
-// FFT twiddle buffer (fft.cuh twf / twi): kM forward entries (level s,
-// block b at (1 << s) - 1 + b), then kM/2 inverse entries.
+// FFT twiddle buffer (fft.cuh twf / twi): forward entries of level s at
+// fwd_base(s) (the sibling levels 4, 5, 7, 9 keep only their even blocks),
+// then kM/2 inverse entries from kM.
+LV_HD constexpr bool fwd_sibling_level(int s) { return s == 4 || s == 5 || s == 7 || s == 9; }
+LV_HD constexpr uint32_t fwd_base(int s) {
+  uint32_t b = 0;
+  for (int q = 0; q < s; ++q) b += fwd_sibling_level(q) ? (1u << q) >> 1 : (1u << q);
+  return b;
+}
 constexpr uint32_t kTwEntries = kM + kM / 2;
 // Spectrum layout of the blind rotation (fft.cuh L_D): register n of
 // thread t = 32 w + L holds DIF output position spec_pos(t, n), bits

@@ -370,7 +370,8 @@ static void pbs_batch(lv_ctx* c, const lv_ct* in, const uint32_t* luts, size_t c
 static void build_tables(lv_ctx* c) {
   const long double PI = 3.141592653589793238462643383279502884L;
   // Linzer-Feig twiddles (c, t) = (cos, tan) rounded from long double
-  // (oracle build_tables): forward level s block b at (1 << s) - 1 + b is
+  // (oracle build_tables): forward level s block b at fwd_base(s) + b (b/2 at
+  // the sibling levels) is
   // zeta^e, e = (kM >> (s+1)) (1 - 4 brv_s(b)) mod 2N, zeta = exp(i pi / N);
   // inverse conj(W^k) = exp(2 pi i k / kM) at kM + k, k < kM/2.
   std::vector<double2> tw(kTwEntries), twist(128);
@@ -380,7 +381,9 @@ static void build_tables(lv_ctx* c) {
       for (uint32_t q = 0; q < s; ++q) r |= ((b >> q) & 1u) << (s - 1 - q);
       const int64_t e = ((int64_t)(kM >> (s + 1)) * (1 - 4 * (int64_t)r)) % (int64_t)(2 * kN);
       const long double ang = PI * (long double)(e < 0 ? e + 2 * kN : e) / (long double)kN;
-      tw[((1u << s) - 1) + b] = make_double2((double)cosl(ang), (double)tanl(ang));
+      if (fwd_sibling_level((int)s) && (b & 1)) continue;  // odd blocks: -i x the even sibling
+      tw[fwd_base((int)s) + (fwd_sibling_level((int)s) ? b >> 1 : b)] =
+          make_double2((double)cosl(ang), (double)tanl(ang));
     }
   for (uint32_t k = 0; k < kM / 2; ++k) {
     const long double ang = 2.0L * PI * (long double)k / (long double)kM;

@@ -58,9 +58,12 @@ struct CtaBar {
 };
 
 // Cross-warp exchanges go through NB shared 16 KB buffers (P polynomials in
-// groups of NB). LVB_XCHG_BUFS=1 trades two barriers per exchange for 16 KB.
+// groups of NB). One buffer (default) costs two barriers per exchange but
+// leaves 16 KB per CTA to L1: at 3 CTAs/SM the carveout drops from 228 to
+// 164 KB and the twiddle tables stay L1-resident (59.4 -> 56.8 ms per 4096
+// PBS; at 2 CTAs/SM it measured slower).
 #ifndef LVB_XCHG_BUFS
-#define LVB_XCHG_BUFS 2
+#define LVB_XCHG_BUFS 1
 #endif
 constexpr int kXchgBufs = LVB_XCHG_BUFS;
 
@@ -372,17 +375,21 @@ __device__ __forceinline__ void dit4_1(double2& x0, double2& x1, double2& x2, do
 }
 
 // Twiddle buffer (context.cu build_tables), Linzer-Feig pairs (c, t):
-//   [0, kM): forward, level s block b at (1 << s) - 1 + b: the negacyclic
-//            root zeta^e, e = (kM >> (s+1)) (1 - 4 brv_s(b)) mod 2N;
+//   [0, kFwdEntries): forward, the negacyclic root zeta^e of level s block b,
+//            e = (kM >> (s+1)) (1 - 4 brv_s(b)) mod 2N, at fwd_base(s) + b —
+//            at the sibling levels 4, 5, 7, 9 only the even blocks, at
+//            fwd_base(s) + b/2 (odd blocks use -i x their even sibling);
 //   [kM, kM + kM/2): inverse, conj(W^k) at kM + k.
-// Levels 0-2 (pass A, blocks fixed by registers) also sit in the constant
-// bank, so those butterflies take their twiddles as constant operands.
+// Compact so the tables (~19 KB touched) stay resident in L1 next to the
+// shared-memory carveout. Levels 0-2 (pass A, blocks fixed by registers)
+// also sit in the constant bank, so those butterflies take their twiddles
+// as constant operands.
 __constant__ double2 c_fwd_a[7];  // defined here: fft.cuh has one includer (kernels.cu)
 __device__ __forceinline__ double2 twf(const double2* __restrict__ tw, int s, uint32_t b) {
 #ifdef LVB_ABL_TW  // timing ablation only
   return make_double2(0.70710678118654757 + s * 1e-3, 0.9 - b * 1e-9);
 #endif
-  return __ldg(tw + ((1u << s) - 1) + b);
+  return __ldg(tw + fwd_base(s) + (fwd_sibling_level(s) ? b >> 1 : b));
 }
 __device__ __forceinline__ double2 twi(const double2* __restrict__ tw, uint32_t k) {
 #ifdef LVB_ABL_TW
