@@ -374,7 +374,7 @@ static void build_tables(lv_ctx* c) {
   // the sibling levels) is
   // zeta^e, e = (kM >> (s+1)) (1 - 4 brv_s(b)) mod 2N, zeta = exp(i pi / N);
   // inverse conj(W^k) = exp(2 pi i k / kM) at kM + k, k < kM/2.
-  std::vector<double2> tw(kTwEntries), twist(128);
+  std::vector<double2> tw(kTwEntries), twist(128 + kM);
   for (uint32_t s = 0; s < kLogM; ++s)
     for (uint32_t b = 0; b < (1u << s); ++b) {
       uint32_t r = 0;  // brv_s(b)
@@ -401,6 +401,15 @@ static void build_tables(lv_ctx* c) {
     coarse[k] = make_double2((double)cosl(ang), (double)sinl(ang));
   }
   set_twist_coarse(coarse);
+  // [128 + x]: the full twist zeta^x = fine[x & 127] * coarse[x >> 7], formed
+  // with the kernels' cmul (fma(a.x, b.x, -(a.y b.y)), fma(a.x, b.y, a.y b.x)),
+  // so a loaded factor equals a formed one bit for bit
+  for (uint32_t j = 0; j < kM; ++j) {
+    const double2 f = twist[j & 127], k = coarse[j >> 7];
+    twist[128 + j] = (j >> 7) == 0 ? f
+                                   : make_double2(std::fma(f.x, k.x, -(f.y * k.y)),
+                                                  std::fma(f.x, k.y, f.y * k.x));
+  }
   LV_CUDA(cudaMalloc(&c->d_tw, tw.size() * sizeof(double2)));
   LV_CUDA(cudaMalloc(&c->d_twist, twist.size() * sizeof(double2)));
   LV_CUDA(cudaMemcpy(c->d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));

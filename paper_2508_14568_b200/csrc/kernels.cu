@@ -212,7 +212,12 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
 #ifndef LVB_TZ_REGS
 #define LVB_TZ_REGS 0  // 1: the 8 twist factors held in registers across the CMUX loop
 #endif
-#if LVB_TZ_REGS
+#ifndef LVB_TWIST_TABLE
+#define LVB_TWIST_TABLE 1  // the untwist factors loaded from the full table (L1-resident) instead of formed
+#endif
+#if LVB_TWIST_TABLE
+#define TWIST_R(r) ((r) == 0 ? tw_fine : __ldg(a.twist + 128 + t + 128 * (r)))
+#elif LVB_TZ_REGS
   double2 tzr[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) tzr[r] = r == 0 ? tw_fine : cmul(tw_fine, c_twist_coarse[r]);
