@@ -280,9 +280,8 @@ def phase_noise(ctx, out, vals):
             "ratio_std_err": float(np.sqrt(2.0 / e.size)) * v / ex}
 
 
-REPORT_FIELDS = ("distance", "visited_cells", "pbs_total", "pbs_equality", "pbs_kernel",
-                 "refresh_count", "preprocessing_pbs", "max_key_variance", "linear_ops",
-                 "half_width")
+REPORT_FIELDS = ("distance", "half_width", "visited_cells", "pbs_total", "pbs_equality",
+                 "pbs_kernel", "refresh_count", "preprocessing_pbs", "max_key_variance")
 
 
 def golden_configs():
@@ -294,7 +293,7 @@ def golden_configs():
 
 
 def report_matches(got, want):
-    """Every RunReport counter of `got` equals the reference's `want`."""
+    """Every RunReport counter (cli.hpp:23-37) of `got` equals the reference's `want`."""
     return all(got[f] == want[f] for f in REPORT_FIELDS)
 
 
