@@ -421,7 +421,11 @@ struct NoHook {
 };
 // hook() runs after the first TMEM trip (the caller issues loads it needs
 // right after the transform there, e.g. the first BSK row).
-template <int P, int NB = kXchgBufs, typename Hook = NoHook, typename Bar = CtaBar>
+// kSyncFirst: buf aliases memory other warps may still be reading when the
+// transform starts (the blind rotation's accumulator): one barrier before
+// the first exchange write.
+template <int P, int NB = kXchgBufs, typename Hook = NoHook, typename Bar = CtaBar,
+          bool kSyncFirst = false>
 __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
                                             const double2* __restrict__ tw, uint32_t t, uint32_t tm,
                                             Hook hook = Hook(), Bar bar = Bar()) {
@@ -450,6 +454,7 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
     double2 w5[2];  // even level-5 blocks 4 b3 + 2 x6; odd ones -i w5
 #pragma unroll
     for (int q = 0; q < 2; ++q) w5[q] = twf(tw, 5, 4 * b3 + 2 * q);
+    if constexpr (kSyncFirst) bar.sync();
     xchg_cta<P, NB>(X, buf, bar, [&](int r) { return t + 128u * r; },
                     [&](int r) { return 16u * r + 128u * (L & 1) + u + 256u * w; });
 #pragma unroll

@@ -167,13 +167,26 @@ __device__ __forceinline__ void own_ld(uint32_t a, int p, int h, uint32_t (&r)[1
       : "memory");
 }
 
+#ifndef LVB_XCHG_ALIAS
+#define LVB_XCHG_ALIAS 0  // 1: measured 56.1 vs 55.86 ms at 3 CTAs/SM, 57.8 at 4 (profiles/r02_lf_variants.txt)
+#endif
+// (throughput kernel only: the exact-mask path re-reads acc in its update)
+constexpr bool kXchgAlias = LVB_XCHG_ALIAS != 0 && LVB_OWN_TMEM != 0 && kXchgBufs * kM * 16 <= 2 * kN * 8;
+
 template <bool kExact>
 __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
+  constexpr bool kAlias = kXchgAlias && !kExact;
   constexpr int kEarly = kExact ? LVB_BSK_EARLY_EXACT : LVB_BSK_EARLY;
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* acc = reinterpret_cast<uint64_t*>(smem);                   // [2][kN]
-  double2* buf = reinterpret_cast<double2*>(smem + 2 * kN * 8);        // [kXchgBufs][kM]
-  uint16_t* ms = reinterpret_cast<uint16_t*>(smem + 2 * kN * 8 + kXchgBufs * kM * 16);
+  // LVB_XCHG_ALIAS: the exchange buffer lives inside the accumulator —
+  // between the decomposition (the last rotated read) and the update
+  // nothing reads acc (the owned coefficients wait in TMEM / registers), so
+  // its 32 KB hold the 16 KB exchange buffer; two barriers fence the
+  // aliasing (before the first exchange write, before the update)
+  double2* buf = kAlias ? reinterpret_cast<double2*>(smem)
+                            : reinterpret_cast<double2*>(smem + 2 * kN * 8);  // [kXchgBufs][kM]
+  uint16_t* ms = reinterpret_cast<uint16_t*>(smem + 2 * kN * 8 + (kAlias ? 0 : kXchgBufs * kM * 16));
   __shared__ uint32_t tmem_slot;
   // TMEM columns: P spectra x 32 (exchange trips); the throughput kernel also
   // parks its owned accumulator coefficients at [64, 128) (LVB_OWN_TMEM)
@@ -268,16 +281,17 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
     double2 bpre[kEarly][kExact ? 6 : 4];
     const double2* bsk_row =
         a.bskf + (size_t)i * (8 * (kExact ? 6 : 4) * 128) + t;
-    fft_forward<2>(X, buf, tw, t, tm, [&] {
+    auto bsk_hook = [&] {
 #pragma unroll
       for (int q = 0; q < kEarly; ++q)
 #pragma unroll
         for (int e = 0; e < (kExact ? 6 : 4); ++e)
           bpre[q][e] = ld_stream<true>(bsk_row + (q * (kExact ? 6 : 4) + e) * 128);
-    });
+    };
+    fft_forward<2, kXchgBufs, decltype(bsk_hook), CtaBar, kAlias>(X, buf, tw, t, tm, bsk_hook);
 #define BSK_AT(q, e, ptr) ((q) < kEarly ? bpre[(q) < kEarly ? (q) : 0][e] : ld_stream<true>(ptr))
 #else
-    fft_forward<2>(X, buf, tw, t, tm);
+    fft_forward<2, kXchgBufs, NoHook, CtaBar, kAlias>(X, buf, tw, t, tm);
 #define BSK_AT(q, e, ptr) ld_stream<true>(ptr)
 #endif
 
@@ -302,6 +316,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         Z[2][q] = mac2(d1, b1, d0, b0);  // body output: row 1 first
       }
       fft_inverse_a<3>(Z, buf, tw, t, tm);
+      if constexpr (kAlias) __syncthreads();  // every warp's exchange reads precede the update
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const double2 tv = TWIST_R(r);
@@ -330,6 +345,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         X[1][q] = mac2(d1, b11, d0, b01);  // output o: row o first
       }
       fft_inverse_a<2>(X, buf, tw, t, tm);
+      if constexpr (kAlias) __syncthreads();  // every warp's exchange reads precede the update
 #if LVB_OWN_TMEM
 #pragma unroll
       for (int h = 0; h < 2; ++h) {  // r in [4h, 4h + 4): own[p][8h .. 8h + 7]
@@ -402,8 +418,8 @@ __global__ void __launch_bounds__(128, 2) blind_rotate_exact_kernel(BrArgs a) {
   blind_rotate_body<true>(a);
 }
 
-size_t blind_rotate_smem_bytes(uint32_t n, bool) {
-  return 2 * kN * 8 + kXchgBufs * kM * 16 + ((n + 1) * 2 + 15) / 16 * 16;
+size_t blind_rotate_smem_bytes(uint32_t n, bool exact) {
+  return 2 * kN * 8 + (kXchgAlias && !exact ? 0 : kXchgBufs * kM * 16) + ((n + 1) * 2 + 15) / 16 * 16;
 }
 
 // ------------------------------------------------------- BR, CTA pair
