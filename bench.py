@@ -140,26 +140,31 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def host_has_avx2_fma() -> bool:
+def host_has_avx512() -> bool:
+    """The fast oracle build (x86-64-v4) needs AVX-512F/DQ/BW/VL + FMA."""
     try:
-        flags = open("/proc/cpuinfo").read().split()
-        return "avx2" in flags and "fma" in flags
+        flags = set(open("/proc/cpuinfo").read().split())
+        return {"avx512f", "avx512dq", "avx512bw", "avx512vl", "fma"} <= flags
     except OSError:
         return False
 
 
 def cpu_oracle_pbs_rate(sample: int, threads: int = 0):
-    """The oracle's PBS on host cores (kind 'port'): `sample` cfg2 items, on
-    the -O3 x86-64-v3 build of the oracle (hardware FMA; bit-identical to the
-    -O2 checker build) when the host supports it."""
+    """The oracle's PBS on host cores (kind 'port'): `sample` cfg2 items on the
+    -O3 x86-64-v4 build, 8 ciphertexts per AVX-512 lane set
+    (orc_pbs_batch_simd; bit-identical to the -O2 checker build) when the
+    host supports it, else the scalar checker."""
     from oracle import oracle as O
     from paper_2508_14568_b200 import workloads as W
-    o = O.Oracle(0, threads=threads, fast=host_has_avx2_fma())
+    fast = host_has_avx512()
+    o = O.Oracle(0, threads=threads, fast=fast)
     vals = W.cfg2()[:sample]
     rows = np.stack([o.encrypt(v, i) for i, v in enumerate(vals)])
     luts = np.tile(np.arange(16, dtype=np.int32), (sample, 1))
     t0 = time.perf_counter()
-    out = o.pbs_batch(rows, luts, 0, threads)
+    out = o.pbs_batch_simd(rows, luts, threads) if fast else None
+    if out is None:
+        out = o.pbs_batch(rows, luts, 0, threads)
     dt = time.perf_counter() - t0
     ok = all(o.decrypt(out[i]) == vals[i] for i in range(sample))
     cores = threads if threads > 0 else (os.cpu_count() or 1)
@@ -234,7 +239,7 @@ def run_reference(args, ws, rank):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    sample = min(4096, 32 * threads)
+    sample = min(4096, 64 * threads)
     # each step: a bounded sample of the cfg2 batch on all host threads
     for _ in range(max(1, min(args.warmup, 1))):
         cpu_oracle_pbs_rate(min(sample, 16), threads)
@@ -252,8 +257,8 @@ def run_reference(args, ws, rank):
                    "sample_per_step": sample},
         "cpu_baseline": {"value": v, "unit": "PBS/s", "cores": threads, "kind": "port",
                          "sample": f"{sample} of the 4096 cfg2 PBS per step on {threads} threads "
-                                   "(oracle/tfhe_oracle.c, the CPU restatement, -O3 x86-64-v3 "
-                                   f"build={host_has_avx2_fma()}; the reference's SimBackend "
+                                   "(oracle/tfhe_oracle.c, the CPU restatement, -O3 x86-64-v4, 8 PBS per AVX-512 "
+                                   f"lane set: {host_has_avx512()}; the reference's SimBackend "
                                    "performs no cryptography, see reference_sim)"},
         "e2e": {"value": v, "unit": "PBS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "context": cpu_context(threads, v),
@@ -507,7 +512,7 @@ def main():
         except Exception as e:  # reported, never silently dropped
             line["dp_cells"] = {"error": repr(e)}
         try:
-            sample = min(4096, 128 * (os.cpu_count() or 1))  # ~10 s of host work
+            sample = min(4096, 256 * (os.cpu_count() or 1))  # ~10 s of host work
             r, cores, dt, ok, rows_o, out_o = cpu_oracle_pbs_rate(sample)
             # the same ciphertexts through the product path (C ABI, host
             # buffers): every output LWE must equal the oracle's bit for bit
@@ -515,8 +520,8 @@ def main():
             same = int(np.sum(np.all(got == out_o, axis=1)))
             line["cpu_baseline"] = {"value": r, "unit": "PBS/s", "cores": cores, "kind": "port",
                                     "sample": f"{sample} of the 4096 cfg2 PBS on {cores} threads "
-                                              f"in {dt:.1f}s (oracle/tfhe_oracle.c, -O3 x86-64-v3 "
-                                              f"build={host_has_avx2_fma()}), correct={ok}",
+                                              f"in {dt:.1f}s (oracle/tfhe_oracle.c, -O3 x86-64-v4, 8 PBS per AVX-512 "
+                                              f"lane set: {host_has_avx512()}), correct={ok}",
                                     "bit_exact": f"{same}/{sample}",
                                     "context": cpu_context(cores, r),
                                     "bit_exact_note": "GPU PBS outputs (lv_pbs_batch_host) on the "

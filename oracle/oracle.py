@@ -90,6 +90,8 @@ def lib(fast: bool = False):
         L.orc_fft_phase_error_var.restype = ctypes.c_double
         L.orc_fft_phase_error_var.argtypes = [vp, u32p, u64p]
         L.orc_pbs_batch.argtypes = [vp, ctypes.c_size_t, u64p, i32p, u64p, ctypes.c_int, ctypes.c_int]
+        L.orc_pbs_batch_simd.restype = ctypes.c_int
+        L.orc_pbs_batch_simd.argtypes = [vp, ctypes.c_size_t, u64p, i32p, u64p, ctypes.c_int]
         L.orc_fft_forward_i64.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double)]
         L.orc_fft_backward_torus.argtypes = [vp, ctypes.POINTER(ctypes.c_double), u64p]
         _libs[fast] = L
@@ -240,6 +242,18 @@ class Oracle:
         self._L.orc_pbs_batch(self._c, cts.shape[0], _p(cts, ctypes.c_uint64),
                             _p(luts, ctypes.c_int32), _p(out, ctypes.c_uint64), mode, threads)
         return out
+
+    def pbs_batch_simd(self, cts: np.ndarray, luts: np.ndarray, threads: int = 0):
+        """The CPU baseline's lane-vectorised PBS (8 ciphertexts per AVX-512
+        lane set; only in the fast build): bit-identical to pbs_batch.
+        None when unavailable (scalar build, or parameters it does not cover)."""
+        cts = np.ascontiguousarray(cts, np.uint64).reshape(-1, self.big)
+        luts = np.ascontiguousarray(luts, np.int32).reshape(-1, 16)
+        assert cts.shape[0] == luts.shape[0]
+        out = np.zeros_like(cts)
+        rc = self._L.orc_pbs_batch_simd(self._c, cts.shape[0], _p(cts, ctypes.c_uint64),
+                                        _p(luts, ctypes.c_int32), _p(out, ctypes.c_uint64), threads)
+        return out if rc == 0 else None
 
     def fft_forward(self, poly: np.ndarray) -> np.ndarray:
         poly = np.ascontiguousarray(poly, np.int64)

@@ -982,3 +982,290 @@ void orc_blind_rotate_batch(const orc_ctx* c, size_t count, const uint32_t* ms,
   br_batch_arg a = {c, ms, tp, glwe_out, mode};
   parallel_for(count, threads, br_range, &a);
 }
+
+/* ------------------------------------------------------------------ */
+/* CPU-baseline build only: the same KS_PBS, 8 ciphertexts in lockstep, one */
+/* per AVX-512 lane (the FFT, MAC and conversions vectorised across the     */
+/* batch, the KSK streamed once per 8 ciphertexts). Every lane performs     */
+/* exactly the scalar path's IEEE operations (vfmadd/vfnmadd are single-    */
+/* rounding fma, the torus conversion is rint + fix-up + nearest-even), so  */
+/* outputs are bit-identical to orc_pbs (checked by tests/test_oracle_     */
+/* pins.py). FFT-spec mode (mode 0) and default-layout keys only.           */
+#if defined(__AVX512F__) && defined(__AVX512DQ__)
+#include <immintrin.h>
+#define W8 8
+
+typedef struct {
+  __m512d re, im;
+} v8c;
+
+static inline void v_ct_lf(v8c* u, v8c* v, const double* w) {
+  const __m512d c = _mm512_set1_pd(w[0]), t = _mm512_set1_pd(w[1]);
+  const __m512d a = _mm512_fnmadd_pd(t, v->im, v->re); /* fma(-t, v.im, v.re) */
+  const __m512d b = _mm512_fmadd_pd(t, v->re, v->im);
+  const v8c U = *u;
+  u->re = _mm512_fmadd_pd(c, a, U.re);
+  u->im = _mm512_fmadd_pd(c, b, U.im);
+  v->re = _mm512_fnmadd_pd(c, a, U.re);
+  v->im = _mm512_fnmadd_pd(c, b, U.im);
+}
+static inline void v_ct_lf_mi(v8c* u, v8c* v, const double* w) { /* (-i w) v = c (b - i a) */
+  const __m512d c = _mm512_set1_pd(w[0]), t = _mm512_set1_pd(w[1]);
+  const __m512d a = _mm512_fnmadd_pd(t, v->im, v->re);
+  const __m512d b = _mm512_fmadd_pd(t, v->re, v->im);
+  const v8c U = *u;
+  u->re = _mm512_fmadd_pd(c, b, U.re);
+  u->im = _mm512_fnmadd_pd(c, a, U.im);
+  v->re = _mm512_fnmadd_pd(c, b, U.re);
+  v->im = _mm512_fmadd_pd(c, a, U.im);
+}
+static inline void v_ct_lf_i(v8c* u, v8c* v, const double* w) { /* (i w) v = c (-b + i a) */
+  const __m512d c = _mm512_set1_pd(w[0]), t = _mm512_set1_pd(w[1]);
+  const __m512d a = _mm512_fnmadd_pd(t, v->im, v->re);
+  const __m512d b = _mm512_fmadd_pd(t, v->re, v->im);
+  const v8c U = *u;
+  u->re = _mm512_fnmadd_pd(c, b, U.re);
+  u->im = _mm512_fmadd_pd(c, a, U.im);
+  v->re = _mm512_fmadd_pd(c, b, U.re);
+  v->im = _mm512_fnmadd_pd(c, a, U.im);
+}
+
+static void v_fft_fwd(const orc_ctx* c, v8c* x) {
+  const uint32_t M = c->M;
+  for (uint32_t s = 0; s < c->logM; ++s) {
+    const uint32_t half = M >> (s + 1);
+    const int sib = c->logM == 10 && (s == 4 || s == 5 || s == 7 || s == 9);
+    for (uint32_t b = 0; b < (1u << s); ++b) {
+      const int mi = sib && (b & 1u);
+      const double* w = c->fwd_lf + 2 * ((1u << s) - 1 + (mi ? b - 1 : b));
+      v8c* blk = x + 2 * half * b;
+      for (uint32_t j = 0; j < half; ++j) {
+        if (mi)
+          v_ct_lf_mi(blk + j, blk + j + half, w);
+        else
+          v_ct_lf(blk + j, blk + j + half, w);
+      }
+    }
+  }
+}
+
+static void v_fft_inv(const orc_ctx* c, v8c* x) {
+  const uint32_t M = c->M;
+  for (int s = (int)c->logM - 1; s >= 0; --s) {
+    const uint32_t half = M >> (s + 1);
+    for (uint32_t blk = 0; blk < M; blk += 2 * half)
+      for (uint32_t j = 0; j < half; ++j) {
+        const uint32_t k = j << s;
+        v8c* u = x + blk + j;
+        v8c* v = x + blk + j + half;
+        if (half <= 2) {
+          const v8c U = *u, V = *v;
+          if (k == 0) {
+            u->re = _mm512_add_pd(U.re, V.re);
+            u->im = _mm512_add_pd(U.im, V.im);
+            v->re = _mm512_sub_pd(U.re, V.re);
+            v->im = _mm512_sub_pd(U.im, V.im);
+          } else { /* u +- i v */
+            u->re = _mm512_sub_pd(U.re, V.im);
+            u->im = _mm512_add_pd(U.im, V.re);
+            v->re = _mm512_add_pd(U.re, V.im);
+            v->im = _mm512_sub_pd(U.im, V.re);
+          }
+        } else if (c->logM == 10 && s != 2 && s != 5 && s != 7 && k >= M / 4) {
+          v_ct_lf_i(u, v, c->inv_lf + 2 * (k - M / 4));
+        } else {
+          v_ct_lf(u, v, c->inv_lf + 2 * k);
+        }
+      }
+  }
+}
+
+/* f64_to_torus per lane: r = rint(y 2^-64), d = y - r 2^64 (exact), d >= 2^63
+ * -> d - 2^64, then llrint (nearest-even, the default MXCSR mode). */
+static inline __m512i v_f64_to_torus(__m512d y) {
+  const __m512d two64 = _mm512_set1_pd(18446744073709551616.0);
+  const __m512d r = _mm512_roundscale_pd(_mm512_mul_pd(y, _mm512_set1_pd(0x1p-64)),
+                                         _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC);
+  __m512d d = _mm512_sub_pd(y, _mm512_mul_pd(r, two64));
+  const __mmask8 big = _mm512_cmp_pd_mask(d, _mm512_set1_pd(9223372036854775808.0), _CMP_GE_OQ);
+  d = _mm512_mask_sub_pd(d, big, d, two64);
+  return _mm512_cvtpd_epi64(d);
+}
+
+typedef struct {
+  uint64_t* acc;   /* [(k+1) N][W8]: the 8 accumulators lane-interleaved */
+  v8c* spec;       /* [rows][M] */
+  v8c* facc;       /* [M] */
+  uint64_t* small; /* [W8][n+1] */
+  uint32_t* ms;    /* [W8][n+1] */
+  uint64_t* tp;    /* [N] */
+} v_scratch;
+
+/* the 8 ciphertexts in[w] (count <= 8 real ones; the rest repeat lane 0) */
+static void v_pbs8(const orc_ctx* c, const uint64_t* const* in, const int32_t* const* luts,
+                   uint64_t* const* out, int count, v_scratch* sc) {
+  const orc_params* p = &c->p;
+  const uint32_t N = p->N, k = p->k, n = p->n, M = c->M, L = p->ks_level, rows = rows_of(p);
+  const uint32_t kN = k * N;
+  /* key switch: the KSK row of (j, l) serves all 8 ciphertexts */
+  for (int w = 0; w < W8; ++w) {
+    uint64_t* o = sc->small + (size_t)w * (n + 1);
+    memset(o, 0, sizeof(uint64_t) * n);
+    o[n] = in[w][kN];
+  }
+  int64_t dig[W8][64];
+  for (uint32_t j = 0; j < kN; ++j) {
+    for (int w = 0; w < W8; ++w) decompose(in[w][j], p->ks_base_log, L, dig[w]);
+    for (uint32_t l = 0; l < L; ++l) {
+      const uint64_t* row = c->ksk + ((size_t)j * L + l) * (n + 1);
+      for (int w = 0; w < W8; ++w) {
+        if (!dig[w][l]) continue;
+        const __m512i d = _mm512_set1_epi64(dig[w][l]);
+        uint64_t* o = sc->small + (size_t)w * (n + 1);
+        uint32_t cc = 0;
+        for (; cc + 8 <= n + 1; cc += 8) {
+          const __m512i r = _mm512_loadu_si512((const void*)(row + cc));
+          const __m512i v = _mm512_loadu_si512((const void*)(o + cc));
+          _mm512_storeu_si512((void*)(o + cc), _mm512_sub_epi64(v, _mm512_mullo_epi64(d, r)));
+        }
+        for (; cc <= n; ++cc) o[cc] -= (uint64_t)dig[w][l] * row[cc];
+      }
+    }
+  }
+  /* ACC = X^{-b~} (0, TP), lane-interleaved */
+  memset(sc->acc, 0, sizeof(uint64_t) * W8 * (size_t)k * N);
+  for (int w = 0; w < W8; ++w) {
+    orc_modswitch(c, sc->small + (size_t)w * (n + 1), sc->ms + (size_t)w * (n + 1));
+    orc_test_poly(c, luts[w], sc->tp);
+    const uint32_t e = (2 * N - sc->ms[(size_t)w * (n + 1) + n]) % (2 * N);
+    for (uint32_t j = 0; j < N; ++j) {
+      const uint32_t t = (j + 2 * N - e) % (2 * N);
+      sc->acc[((size_t)k * N + j) * W8 + w] = t < N ? sc->tp[t] : (uint64_t)0 - sc->tp[t - N];
+    }
+  }
+  const __m512i lane = _mm512_setr_epi64(0, 1, 2, 3, 4, 5, 6, 7);
+  const __m512i half41 = _mm512_set1_epi64((int64_t)1 << 40);
+  for (uint32_t i = 0; i < n; ++i) {
+    /* per-lane rotation a_w: rotated difference, 1-level base-2^23 digit
+     * (decompose: (x + 2^40) >> 41, centred), folded into the spectra */
+    int64_t av[W8];
+    for (int w = 0; w < W8; ++w) av[w] = sc->ms[(size_t)w * (n + 1) + i];
+    const __m512i a = _mm512_loadu_si512((const void*)av);
+    for (uint32_t comp = 0; comp <= k; ++comp) {
+      const uint64_t* P = sc->acc + (size_t)comp * N * W8;
+      double* sp = (double*)(sc->spec + (size_t)comp * M);
+      for (uint32_t j = 0; j < N; ++j) {
+        /* t = (j - a) mod 2N; rv = t < N ? P[t] : -P[t - N] */
+        __m512i t = _mm512_sub_epi64(_mm512_set1_epi64(j + 2 * N), a);
+        t = _mm512_and_si512(t, _mm512_set1_epi64(2 * N - 1));
+        const __mmask8 wrap = _mm512_cmpge_epu64_mask(t, _mm512_set1_epi64(N));
+        const __m512i src = _mm512_mask_sub_epi64(t, wrap, t, _mm512_set1_epi64(N));
+        const __m512i idx = _mm512_add_epi64(_mm512_slli_epi64(src, 3), lane);
+        __m512i rv = _mm512_i64gather_epi64(idx, (const void*)P, 8);
+        rv = _mm512_mask_sub_epi64(rv, wrap, _mm512_setzero_si512(), rv);
+        const __m512i x = _mm512_sub_epi64(rv, _mm512_loadu_si512((const void*)(P + (size_t)j * W8)));
+        const __m512i v = _mm512_srli_epi64(_mm512_add_epi64(x, half41), 41);
+        const __m512i d = _mm512_srai_epi64(_mm512_slli_epi64(v, 41), 41); /* centred 23-bit digit */
+        const uint32_t jj = j < M ? j : j - M;
+        _mm512_storeu_pd(sp + (size_t)jj * 16 + (j < M ? 0 : 8), _mm512_cvtepi64_pd(d));
+      }
+    }
+    for (uint32_t r = 0; r < rows; ++r) v_fft_fwd(c, sc->spec + (size_t)r * M);
+    for (uint32_t o = 0; o <= k; ++o) {
+      for (uint32_t f = 0; f < M; ++f) {
+        __m512d ar = _mm512_setzero_pd(), ai = _mm512_setzero_pd();
+        for (uint32_t rr = 0; rr < rows; ++rr) {
+          const uint32_t r = (rr + o) % rows;
+          const v8c dd = sc->spec[(size_t)r * M + f];
+          const double* b = c->bskf + ((i * rows + r) * (k + 1) + o) * 2 * M + 2 * f;
+          const __m512d br = _mm512_set1_pd(b[0]), bi = _mm512_set1_pd(b[1]);
+          ar = _mm512_fmadd_pd(dd.re, br, ar);
+          ar = _mm512_fnmadd_pd(dd.im, bi, ar);
+          ai = _mm512_fmadd_pd(dd.re, bi, ai);
+          ai = _mm512_fmadd_pd(dd.im, br, ai);
+        }
+        sc->facc[f].re = ar;
+        sc->facc[f].im = ai;
+      }
+      v_fft_inv(c, sc->facc);
+      uint64_t* A = sc->acc + (size_t)o * N * W8;
+      for (uint32_t j = 0; j < M; ++j) {
+        const __m512d ur = _mm512_set1_pd(c->untwist[2 * j]), ui = _mm512_set1_pd(c->untwist[2 * j + 1]);
+        const v8c z = sc->facc[j];
+        const __m512d t1 = _mm512_mul_pd(z.im, ui), t2 = _mm512_mul_pd(z.im, ur);
+        const __m512d re = _mm512_fmsub_pd(z.re, ur, t1); /* fma(ar, br, -t1) */
+        const __m512d im = _mm512_fmadd_pd(z.re, ui, t2);
+        uint64_t* a0 = A + (size_t)j * W8;
+        uint64_t* a1 = A + (size_t)(j + M) * W8;
+        _mm512_storeu_si512((void*)a0, _mm512_add_epi64(_mm512_loadu_si512((const void*)a0), v_f64_to_torus(re)));
+        _mm512_storeu_si512((void*)a1, _mm512_add_epi64(_mm512_loadu_si512((const void*)a1), v_f64_to_torus(im)));
+      }
+    }
+  }
+  /* sample extract per lane */
+  for (int w = 0; w < count; ++w) {
+    uint64_t* o = out[w];
+    for (uint32_t q = 0; q < k; ++q) {
+      const uint64_t* A = sc->acc + (size_t)q * N * W8;
+      o[(size_t)q * N] = A[w];
+      for (uint32_t j = 1; j < N; ++j) o[(size_t)q * N + j] = (uint64_t)0 - A[(size_t)(N - j) * W8 + w];
+    }
+    o[(size_t)k * N] = sc->acc[(size_t)k * N * W8 + w];
+  }
+}
+
+typedef struct {
+  const orc_ctx* c;
+  const uint64_t* in;
+  const int32_t* luts;
+  uint64_t* out;
+  size_t count;
+} v_batch_arg;
+
+static void v_range(void* a, size_t lo, size_t hi) { /* lo, hi: group indices */
+  v_batch_arg* b = (v_batch_arg*)a;
+  const orc_params* p = &b->c->p;
+  const size_t len = (size_t)p->k * p->N + 1;
+  v_scratch sc;
+  sc.acc = (uint64_t*)aligned_alloc(64, sizeof(uint64_t) * W8 * (p->k + 1) * p->N);
+  sc.tp = (uint64_t*)malloc(sizeof(uint64_t) * p->N);
+  sc.spec = (v8c*)aligned_alloc(64, sizeof(v8c) * rows_of(p) * b->c->M);
+  sc.facc = (v8c*)aligned_alloc(64, sizeof(v8c) * b->c->M);
+  sc.small = (uint64_t*)malloc(sizeof(uint64_t) * W8 * (p->n + 1));
+  sc.ms = (uint32_t*)malloc(sizeof(uint32_t) * W8 * (p->n + 1));
+  for (size_t g = lo; g < hi; ++g) {
+    const uint64_t* in[W8];
+    const int32_t* luts[W8];
+    uint64_t* out[W8];
+    const size_t base = g * W8;
+    const int count = (int)(b->count - base < W8 ? b->count - base : W8);
+    for (int w = 0; w < W8; ++w) {
+      const size_t t = base + (size_t)(w < count ? w : 0);
+      in[w] = b->in + t * len;
+      luts[w] = b->luts + 16 * t;
+      out[w] = b->out + t * len;
+    }
+    v_pbs8(b->c, in, luts, out, count, &sc);
+  }
+  free(sc.acc);
+  free(sc.spec);
+  free(sc.facc);
+  free(sc.small);
+  free(sc.ms);
+  free(sc.tp);
+}
+
+int orc_pbs_batch_simd(const orc_ctx* c, size_t count, const uint64_t* in, const int32_t* luts,
+                       uint64_t* out, int threads) {
+  if (c->p.pbs_level != 1 || c->p.exact_mask_product) return -1;
+  v_batch_arg a = {c, in, luts, out, count};
+  parallel_for((count + W8 - 1) / W8, threads, v_range, &a);
+  return 0;
+}
+#else
+int orc_pbs_batch_simd(const orc_ctx* c, size_t count, const uint64_t* in, const int32_t* luts,
+                       uint64_t* out, int threads) {
+  (void)c, (void)count, (void)in, (void)luts, (void)out, (void)threads;
+  return -1; /* built without AVX-512 */
+}
+#endif

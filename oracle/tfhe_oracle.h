@@ -115,6 +115,11 @@ void orc_pbs(const orc_ctx* c, const uint64_t* in_big, const int32_t lut[16],
  * count*16 entries. */
 void orc_pbs_batch(const orc_ctx* c, size_t count, const uint64_t* in_big,
                    const int32_t* luts, uint64_t* out_big, int mode, int threads);
+/* CPU-baseline build (AVX-512): the same PBS, 8 ciphertexts per vector lane
+ * set, bit-identical outputs; returns -1 when built without AVX-512 or for
+ * parameters it does not cover (pbs_level != 1, exact-mask keys). */
+int orc_pbs_batch_simd(const orc_ctx* c, size_t count, const uint64_t* in_big,
+                       const int32_t* luts, uint64_t* out_big, int threads);
 
 /* Negacyclic f64 transform pieces, for unit tests of the FFT spec. */
 void orc_fft_forward_i64(const orc_ctx* c, const int64_t* poly, double* spec);

@@ -91,3 +91,27 @@ def test_golden_distances_equal_wagner_fischer(golden):
         if "error" in c or c["mode"] != "exact":
             continue
         assert c["report"]["distance"] == W.wf_distance(c["a"], c["b"]) % 32
+
+
+def _has_avx512():
+    try:
+        flags = set(open("/proc/cpuinfo").read().split())
+    except OSError:
+        return False
+    return {"avx512f", "avx512dq", "avx512bw", "avx512vl", "fma"} <= flags
+
+
+@pytest.mark.skipif(not _has_avx512(), reason="the CPU-baseline build needs AVX-512")
+def test_cpu_baseline_build_bit_identical():
+    """The CPU baseline (the -O3 x86-64-v4 oracle build, 8 ciphertexts per
+    AVX-512 lane set) equals the scalar checker bit for bit, on a ragged
+    batch (11 = 8 + 3 lanes) with two LUTs."""
+    import numpy as np
+    from oracle import oracle as O
+    slow, fast = O.Oracle(0), O.Oracle(0, fast=True)
+    rows = np.stack([slow.encrypt(v % 32, 500 + v) for v in range(11)])
+    luts = np.tile(np.arange(16, dtype=np.int32), (11, 1))
+    luts[1::2] = np.array([(3 * x + 1) % 16 for x in range(16)], np.int32)
+    want = slow.pbs_batch(rows, luts)
+    assert np.array_equal(fast.pbs_batch(rows, luts), want)
+    assert np.array_equal(fast.pbs_batch_simd(rows, luts), want)
