@@ -51,6 +51,9 @@ static BandSpec to_band(const lv_band* b) {
   return s;
 }
 
+// Wave descriptors uploaded per chunk (76 B each: ~160 MB of device memory).
+constexpr size_t kWaveChunkItems = size_t(1) << 21;
+
 // Plan cache bound: ~24 B per cell, so 8M cells is ~200 MB of host memory.
 constexpr uint64_t kPlanCacheCells = 8u << 20;
 
@@ -309,28 +312,18 @@ static void run_traversals(lv_ctx* c, const std::vector<PairIn>& pairs, uint32_t
     runs[p] = r;
   }
 
-  // flatten + single upload
-  std::vector<LinDesc> d;
-  std::vector<uint32_t> l;
-  std::vector<BrOut> o;
+  // flatten and launch in chunks of whole waves: each chunk's descriptors are
+  // uploaded into the reused device buffers and its launch sequence replayed
+  // as one CUDA graph, so device memory for descriptors stays bounded
+  // (kWaveChunkItems) however many pairs a batch holds; chunks run in wave
+  // order on the context stream.
   struct Launch {
     size_t off, count;
   };
-  std::vector<Launch> launches;
   uint64_t total_items = 0;
-  for (auto& kv : waves) {
-    for (auto* part : {&kv.second.pre, &kv.second.main}) {
-      if (part->empty()) continue;
-      launches.push_back({d.size(), part->size()});
-      for (const PbsItem& it : *part) {
-        d.push_back(it.in);
-        l.push_back(it.lut);
-        o.push_back(it.out);
-      }
-      total_items += part->size();
-    }
-  }
-  if (!d.empty()) {
+  auto flush = [&](std::vector<LinDesc>& d, std::vector<uint32_t>& l, std::vector<BrOut>& o,
+                   std::vector<Launch>& launches) {
+    if (d.empty()) return;
     LinDesc* dd = c->desc.get(d.size());
     uint32_t* dl = c->lut_item.get(l.size());
     BrOut* dout = c->br_out.get(o.size());
@@ -352,9 +345,35 @@ static void run_traversals(lv_ctx* c, const std::vector<PairIn>& pairs, uint32_t
     LV_CUDA(cudaStreamEndCapture(c->stream, &graph));
     LV_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     LV_CUDA(cudaGraphLaunch(exec, c->stream));
-    LV_CUDA(cudaStreamSynchronize(c->stream));
+    LV_CUDA(cudaStreamSynchronize(c->stream));  // the buffers are reused by the next chunk
     cudaGraphExecDestroy(exec);
     cudaGraphDestroy(graph);
+    d.clear();
+    l.clear();
+    o.clear();
+    launches.clear();
+  };
+  {
+    std::vector<LinDesc> d;
+    std::vector<uint32_t> l;
+    std::vector<BrOut> o;
+    std::vector<Launch> launches;
+    for (auto& kv : waves) {
+      size_t wave_items = kv.second.pre.size() + kv.second.main.size();
+      if (!d.empty() && d.size() + wave_items > kWaveChunkItems) flush(d, l, o, launches);
+      for (auto* part : {&kv.second.pre, &kv.second.main}) {
+        if (part->empty()) continue;
+        launches.push_back({d.size(), part->size()});
+        for (const PbsItem& it : *part) {
+          d.push_back(it.in);
+          l.push_back(it.lut);
+          o.push_back(it.out);
+        }
+        total_items += part->size();
+        std::vector<PbsItem>().swap(*part);  // the host copy is no longer needed
+      }
+    }
+    flush(d, l, o, launches);
   }
 
   // score = trivial(0) + sum of path reads (kernel.cpp:193-200)
