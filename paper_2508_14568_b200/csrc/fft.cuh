@@ -91,6 +91,19 @@ __device__ __forceinline__ void xchg_cta(double2 (&X)[P][8], double2* buf, const
   }
 }
 
+// Phase probes (diagnostic builds, -DLVB_PROBE): lane 0 of each warp of
+// CTA 0 adds the SM clock at mark k; the host turns sums of timestamps into
+// mean phase durations (lv_debug_probe). No-ops in the product.
+#ifdef LVB_PROBE
+__device__ unsigned long long g_probe[4][32];
+__device__ __forceinline__ void probe_mark(int k) {
+  if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
+    atomicAdd(&g_probe[threadIdx.x >> 5][k], (unsigned long long)clock64());
+}
+#else
+__device__ __forceinline__ void probe_mark(int) {}
+#endif
+
 // ---------------------------------------------------------------- TMEM
 // Allocation: warp 0 allocates ncols columns (power of 2, >= 32) and
 // writes the base address to *slot; every thread returns it.
@@ -314,6 +327,18 @@ __device__ __forceinline__ void tm_trip_inv(double2 (&X)[P][8], uint32_t tm) {
 }
 
 // ---------------------------------------------------------------- math
+// int32 -> f64, exact: LVB_I2D_MAGIC builds 2^52 + 2^31 + d in the bits and
+// subtracts it back (one DADD on the FP64 pipe instead of an XU conversion).
+#ifndef LVB_I2D_MAGIC
+#define LVB_I2D_MAGIC 0
+#endif
+__device__ __forceinline__ double i2d(int32_t d) {
+#if LVB_I2D_MAGIC
+  return __dadd_rn(__hiloint2double(0x43300000, (int)((uint32_t)d ^ 0x80000000u)), -4503601774854144.0);
+#else
+  return (double)d;
+#endif
+}
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   const double t1 = __dmul_rn(a.y, b.y);
   const double t2 = __dmul_rn(a.y, b.x);
@@ -444,6 +469,7 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
   for (int p = 0; p < P; ++p)
 #pragma unroll
     for (int r = 0; r < 8; r += 2) ct(X[p][r], X[p][r + 1], c_fwd_a[3 + (r >> 1)]);
+  probe_mark(2);
   // L_A -> L_B (cross-warp); pass B (L_B: regs (x4, x5, x6), lanes (x7,
   // x0..x3), warps (x8, x9)): level 3 on x6, block b3 = x >> 7 = 2 w + L0;
   // level 4 on x5, block 2 b3 + x6; level 5 on x4, block 4 b3 + (x5, x6)
@@ -457,6 +483,7 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
     if constexpr (kSyncFirst) bar.sync();
     xchg_cta<P, NB>(X, buf, bar, [&](int r) { return t + 128u * r; },
                     [&](int r) { return 16u * r + 128u * (L & 1) + u + 256u * w; });
+    probe_mark(3);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -487,7 +514,9 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
       w6[q] = twf(tw, 6, b6 + 4 * q);
       w7[q] = twf(tw, 7, 2 * (b6 + 4 * q));
     }
+    probe_mark(4);
     tm_trip_fwd<P>(X, tm);
+    probe_mark(5);
     hook();
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -512,7 +541,9 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
       w8[q] = twf(tw, 8, b8 + 16 * q);
       w9[q] = twf(tw, 9, 2 * (b8 + 16 * q));
     }
+    probe_mark(6);
     tm_trip_fwd<P>(X, tm);
+    probe_mark(7);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -549,7 +580,9 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
   {
     const uint32_t j = L >> 3;
     const double2 v7 = twi(tw, j << 7), v6 = twi(tw, j << 6);  // stage 6, x2 = 1: i v6
+    probe_mark(10);
     tm_trip_inv<P>(X, tm);
+    probe_mark(11);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -570,7 +603,9 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
     double2 v3[2];  // stage 3 per x4; x5 = 1: i v3
 #pragma unroll
     for (int q = 0; q < 2; ++q) v3[q] = twi(tw, (u << 3) + 128 * q);
+    probe_mark(12);
     tm_trip_inv<P>(X, tm);
+    probe_mark(13);
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -596,9 +631,11 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
   double2 v0[2];  // stage 0 per x7; x8 = 1: i v0
 #pragma unroll
   for (int q = 0; q < 2; ++q) v0[q] = twi(tw, t + 128 * q);
+  probe_mark(14);
   bar.sync();
   xchg_cta<P, NB>(X, buf, bar, [&](int r) { return 16u * r + 128u * (L & 1) + u + 256u * w; },
                   [&](int r) { return t + 128u * r; });
+  probe_mark(15);
 #pragma unroll
   for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -626,8 +663,16 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
 // every bit) differs from the oracle's rint only on exact ties, where it
 // yields d = -2^63 instead of +2^63 - 2^64 — the same residue — so no tie
 // fix-up is needed, and d = y - r 2^64 is one exact FMA.
+#ifndef LVB_FLOOR_MAGIC
+#define LVB_FLOOR_MAGIC 0
+#endif
 __device__ __forceinline__ uint64_t f64_to_torus(double y) {
+#if LVB_FLOOR_MAGIC  // floor by a round-down add of 1.5 * 2^52 (FP64 pipe instead of XU): exact
+  const double C = 6755399441055744.0;
+  const double r = __dadd_rn(__dadd_rd(__fma_rn(y, 0x1p-64, 0.5), C), -C);
+#else
   const double r = floor(__fma_rn(y, 0x1p-64, 0.5));  // the product is exact
+#endif
   const double d = __fma_rn(-r, 18446744073709551616.0, y);
   return (uint64_t)__double2ll_rn(d);
 }

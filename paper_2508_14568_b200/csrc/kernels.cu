@@ -22,6 +22,13 @@ namespace lvb {
 void set_twist_coarse(const double2* host8) {
   cudaMemcpyToSymbol(c_twist_coarse, host8, 8 * sizeof(double2));
 }
+#ifdef LVB_PROBE
+extern "C" int lv_debug_probe(unsigned long long* out128) {  // diagnostic builds only
+  cudaMemcpyFromSymbol(out128, g_probe, sizeof(g_probe));
+  static const unsigned long long zero[4][32] = {};
+  return cudaMemcpyToSymbol(g_probe, zero, sizeof(g_probe));
+}
+#endif
 void set_fwd_consts(const double2* host7) {
   cudaMemcpyToSymbol(c_fwd_a, host7, 7 * sizeof(double2));
 }
@@ -252,6 +259,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
     __syncthreads();
     const uint32_t rot = ms[i];
     if (rot == 0) continue;  // X^0 - 1 = 0: the external product is exactly 0
+    probe_mark(0);
 
     // rotated difference, decomposition, twist (layout fwd A: x = t + 128 r)
     double2 X[2][8];
@@ -269,10 +277,11 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
           const uint64_t rv = s < kN ? pv : (uint64_t)0 - pv;
           d[hpart] = decomp23(rv - own[p][2 * r + hpart]);
         }
-        X[p][r] = make_double2((double)d[0], (double)d[1]);  // the forward transform twists
+        X[p][r] = make_double2(i2d(d[0]), i2d(d[1]));  // the forward transform twists
       }
     }
     if constexpr (!kExact && LVB_OWN_TMEM) own_st(tm + 64, own);
+    probe_mark(1);
 
 #if LVB_BSK_EARLY
     // the first bins' BSK values are requested before the transform's last
@@ -289,6 +298,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
           bpre[q][e] = ld_stream<true>(bsk_row + (q * (kExact ? 6 : 4) + e) * 128);
     };
     fft_forward<2, kXchgBufs, decltype(bsk_hook), CtaBar, kAlias>(X, buf, tw, t, tm, bsk_hook);
+    probe_mark(8);
 #define BSK_AT(q, e, ptr) ((q) < kEarly ? bpre[(q) < kEarly ? (q) : 0][e] : ld_stream<true>(ptr))
 #else
     fft_forward<2, kXchgBufs, NoHook, CtaBar, kAlias>(X, buf, tw, t, tm);
@@ -344,7 +354,9 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         X[0][q] = mac2(d0, b00, d1, b10);
         X[1][q] = mac2(d1, b11, d0, b01);  // output o: row o first
       }
+      probe_mark(9);
       fft_inverse_a<2>(X, buf, tw, t, tm);
+      probe_mark(16);
       if constexpr (kAlias) __syncthreads();  // every warp's exchange reads precede the update
 #if LVB_OWN_TMEM
 #pragma unroll
@@ -391,6 +403,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         }
       }
 #endif
+      probe_mark(17);
     }
   }
 #undef BSK_AT
