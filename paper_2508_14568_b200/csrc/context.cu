@@ -601,6 +601,11 @@ static uint64_t key_fingerprint(lv_ctx* c) {
   return f;
 }
 
+// Carveout preferences (percent of the maximum shared memory; -1 = driver
+// default), measured in profiles/r02_lf_variants.txt.
+constexpr int kPairCarveoutPct = -1;
+constexpr int kBrCarveoutPct = -1;
+
 static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bsk,
                       const uint64_t* ksk, uint64_t key_id, lv_ctx** out) {
   return guard([&] {
@@ -652,6 +657,24 @@ static int create_ctx(const lv_params* params, uint64_t seed, const uint64_t* bs
       LV_CUDA(cudaFuncSetAttribute(blind_rotate_pair_exact_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)blind_rotate_pair_smem_bytes(kMaxLweN)));
+      // Shared-memory carveout preference (percent of the maximum): the rest
+      // of the 256 KB array is L1, which must keep the FFT twiddle tables
+      // (~19 KB touched) resident. -1 leaves the choice to the driver.
+      auto carveout = [](const char* env, int dflt) {
+        const char* e = std::getenv(env);
+        return e ? std::atoi(e) : dflt;
+      };
+      const int pair_pct = carveout("LVB_PAIR_CARVEOUT", kPairCarveoutPct);
+      if (pair_pct >= 0) {
+        LV_CUDA(cudaFuncSetAttribute(blind_rotate_pair_kernel,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, pair_pct));
+        LV_CUDA(cudaFuncSetAttribute(blind_rotate_pair_exact_kernel,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, pair_pct));
+      }
+      const int br_pct = carveout("LVB_BR_CARVEOUT", kBrCarveoutPct);
+      if (br_pct >= 0)
+        LV_CUDA(cudaFuncSetAttribute(blind_rotate_kernel,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, br_pct));
       {
         int sms = 148;
         LV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));

@@ -522,6 +522,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
     __syncthreads();  // previous update of acc visible to the rotated reads
     const uint32_t rot = ms[i];
     if (rot == 0) continue;  // uniform across the pair: both skip
+    probe_mark(0);
 
     // this CMUX's BSK row (slots (t, q), output p), in flight during the
     // forward FFT: row p (this CTA's own polynomial) and row 1 - p
@@ -549,7 +550,9 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
       }
       X[0][r] = make_double2((double)d[0], (double)d[1]);
     }
+    probe_mark(1);
     fft_forward<1, 1>(X, buf, tw, t, tm);
+    probe_mark(8);
     const uint32_t my_full = (uint32_t)__cvta_generic_to_shared(&inbox_full[parity]);
     if (t == 0)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(my_full),
@@ -576,6 +579,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
           "r"(ph)
           : "memory");
     }
+    probe_mark(18);  // spectrum sent and the partner's received
     const double2* other_spec = spec + parity * kM;
     if constexpr (!kExact) {
 #pragma unroll
@@ -628,7 +632,9 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
       }
       continue;
     }
+    probe_mark(9);
     fft_inverse_a<1, 1>(X, buf, tw, t, tm);  // its barriers also order the rotated reads before the update
+    probe_mark(16);
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const double2 ut = make_double2(tz[r].x, -tz[r].y);
@@ -639,6 +645,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
       acc[x] = own[2 * r];
       acc[x + kM] = own[2 * r + 1];
     }
+    probe_mark(17);
   }
   cluster.sync();  // no DSMEM reads of this CTA's buffers remain when it exits
   __syncthreads();

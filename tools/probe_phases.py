@@ -14,10 +14,11 @@ from paper_2508_14568_b200 import workloads as W  # noqa: E402
 NAMES = ["decompose", "fwd pass A", "xchg A->B", "pass B", "trip 1", "pass C", "trip 2",
          "pass D", "MAC", "pass D'", "trip C'", "pass C'", "trip B'", "pass B'",
          "bar+xchg B'->A'", "pass A'", "untwist+torus+update"]
+count = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 c = L.Context(seed=0)
 lib = ctypes.CDLL(os.environ["LVB_LIB"])
 buf = (ctypes.c_ulonglong * 128)()
-vals = W.cfg2()
+vals = W.cfg2()[:count]
 h = c.encrypt(vals)
 ids = np.full(len(vals), c.lut(L.identity_lut()), np.uint32)
 c.bench_pbs(h, ids, 2)
@@ -26,10 +27,16 @@ br, _, _ = c.bench_pbs(h, ids, 1)
 lib.lv_debug_probe(buf)
 a = np.frombuffer(buf, dtype=np.uint64).reshape(4, 32).astype(np.float64)
 ncmux = 880 - 1  # CMUXes with a nonzero rotation are ~all; marks count per CMUX
-print("BR ms", br)
+print("BR ms", br, "items", count)
+# the CTA-pair kernel (small waves) adds mark 18 (spectrum sent, partner's received) after 8
+order = list(range(18)) if count > 148 else [0, 1, 2, 3, 4, 5, 6, 7, 8, 18, 9] + list(range(10, 18))
+names = dict(enumerate(["decompose"] + NAMES[1:8] + ["MAC"] + NAMES[9:]))
+if count <= 148:
+    names[8] = "send + partner wait"
+    names[18] = "MAC"
 tot = np.zeros(4)
-for k, name in enumerate(NAMES):
-    d = (a[:, k + 1] - a[:, k]) / ncmux
+for k0, k1 in zip(order[:-1], order[1:]):
+    d = (a[:, k1] - a[:, k0]) / ncmux
     tot += d
-    print(f"{k:2d}->{k + 1:2d} {name:24s} " + " ".join(f"{x:7.0f}" for x in d))
-print("sum 0->17", " ".join(f"{x:7.0f}" for x in tot))
+    print(f"{k0:2d}->{k1:2d} {names[k0]:24s} " + " ".join(f"{x:7.0f}" for x in d))
+print("sum", " ".join(f"{x:7.0f}" for x in tot))
