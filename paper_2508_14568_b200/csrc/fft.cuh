@@ -433,6 +433,136 @@ __device__ __forceinline__ double2 twist_at(const double2* __restrict__ fine, ui
   return (x >> 7) == 0 ? f : cmul(f, c_twist_coarse[x >> 7]);
 }
 
+// ------------------------------------------------------ twiddle sources
+// Each thread needs the same 22 twiddles every CMUX (they depend only on
+// its position in the layouts): 4 per forward pass B / C / D, 2 for inverse
+// pass C', 4 for B' and A'. TwGlobal loads them from the L1-resident table
+// at every use; TwTmem parks the thread's set in tensor memory once (88
+// columns of its warp's lane quarter, fill()) and fetches a pass's set with
+// one tcgen05.ld — for the latency kernels, where every L1 round trip sits
+// on the critical path. Both give the same values, so results are
+// bit-identical.
+struct TwGlobal {
+  const double2* __restrict__ tw;
+  uint32_t t;
+  __device__ __forceinline__ void fwdB(double2 (&w)[4]) const {
+    const uint32_t L = t & 31, b3 = 2 * (t >> 5) + (L & 1);
+    w[0] = twf(tw, 3, b3);
+    w[1] = twf(tw, 4, 2 * b3);  // odd level-4 blocks: -i w4
+#pragma unroll
+    for (int q = 0; q < 2; ++q) w[2 + q] = twf(tw, 5, 4 * b3 + 2 * q);  // even level-5 blocks
+  }
+  __device__ __forceinline__ void fwdC(double2 (&w)[4]) const {
+    const uint32_t L = t & 31;
+    const uint32_t b6 = 16 * (t >> 5) + 8 * ((L >> 2) & 1) + 2 * ((L >> 1) & 1) + (L & 1);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      w[q] = twf(tw, 6, b6 + 4 * q);
+      w[2 + q] = twf(tw, 7, 2 * (b6 + 4 * q));
+    }
+  }
+  __device__ __forceinline__ void fwdD(double2 (&w)[4]) const {
+    const uint32_t L = t & 31, b8 = 64 * (t >> 5) + 32 * (L >> 4) + (L & 15);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      w[q] = twf(tw, 8, b8 + 16 * q);
+      w[2 + q] = twf(tw, 9, 2 * (b8 + 16 * q));
+    }
+  }
+  __device__ __forceinline__ void invC(double2 (&v)[2]) const {
+    const uint32_t j = (t & 31) >> 3;
+    v[0] = twi(tw, j << 7);
+    v[1] = twi(tw, j << 6);  // stage 6, x2 = 1: i v6
+  }
+  __device__ __forceinline__ void invB(double2 (&v)[4]) const {
+    const uint32_t u = (t & 31) >> 1;
+    v[0] = twi(tw, u << 5);
+    v[1] = twi(tw, u << 4);  // stage 4, x4 = 1: i v4
+#pragma unroll
+    for (int q = 0; q < 2; ++q) v[2 + q] = twi(tw, (u << 3) + 128 * q);  // stage 3 per x4
+  }
+  __device__ __forceinline__ void invA(double2 (&v)[4]) const {
+    v[0] = twi(tw, t << 2);
+    v[1] = twi(tw, t << 1);  // stage 1, x7 = 1: i v1
+#pragma unroll
+    for (int q = 0; q < 2; ++q) v[2 + q] = twi(tw, t + 128 * q);  // stage 0 per x7
+  }
+  template <int K>
+  __device__ __forceinline__ void ready(double2 (&)[K]) const {}
+};
+
+struct TwTmem {
+  uint32_t cols;  // this warp's lane-quarter address of the 88 twiddle columns
+  // column slots: fwd B 0, C 16, D 32, inv C' 48 (8), B' 56, A' 72
+  template <int K>
+  __device__ __forceinline__ void ld(uint32_t c, double2 (&w)[K]) const {
+    uint32_t r[4 * K];
+    if constexpr (K == 4)
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+            "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(cols + c)
+          : "memory");
+    else
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                     "=r"(r[6]), "=r"(r[7])
+                   : "r"(cols + c)
+                   : "memory");
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+      w[q] = make_double2(d_mk(r[4 * q], r[4 * q + 1]), d_mk(r[4 * q + 2], r[4 * q + 3]));
+  }
+  __device__ __forceinline__ void fwdB(double2 (&w)[4]) const { ld(0, w); }
+  __device__ __forceinline__ void fwdC(double2 (&w)[4]) const { ld(16, w); }
+  __device__ __forceinline__ void fwdD(double2 (&w)[4]) const { ld(32, w); }
+  __device__ __forceinline__ void invC(double2 (&v)[2]) const { ld(48, v); }
+  __device__ __forceinline__ void invB(double2 (&v)[4]) const { ld(56, v); }
+  __device__ __forceinline__ void invA(double2 (&v)[4]) const { ld(72, v); }
+  // completes this thread's TMEM loads and fences the twiddle registers
+  template <int K>
+  __device__ __forceinline__ void ready(double2 (&w)[K]) const {
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+      asm volatile("tcgen05.wait::ld.sync.aligned;" : "+d"(w[q].x), "+d"(w[q].y) : : "memory");
+  }
+  // once per CTA: the thread's 22 twiddles from the global table into TMEM
+  __device__ __forceinline__ void fill(const TwGlobal& g) const {
+    double2 a[4];
+    g.fwdB(a);
+    st(0, a);
+    g.fwdC(a);
+    st(16, a);
+    g.fwdD(a);
+    st(32, a);
+    double2 c[2];
+    g.invC(c);
+    st(48, c);
+    g.invB(a);
+    st(56, a);
+    g.invA(a);
+    st(72, a);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  template <int K>
+  __device__ __forceinline__ void st(uint32_t c, const double2 (&w)[K]) const {
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(cols + c + 4 * q),
+                   "r"(d_lo(w[q].x)), "r"(d_hi(w[q].x)), "r"(d_lo(w[q].y)), "r"(d_hi(w[q].y))
+                   : "memory");
+  }
+};
+constexpr uint32_t kTwTmemCols = 88;
+
+__device__ __forceinline__ TwGlobal tw_source(const double2* __restrict__ tw, uint32_t t) {
+  return TwGlobal{tw, t};
+}
+__device__ __forceinline__ TwTmem tw_source(TwTmem s, uint32_t) { return s; }
+
 // ---------------------------------------------------------------- forward
 // Negacyclic forward transform (oracle fft_fwd): level s pairs bit x(9-s)
 // of the position, block b = x >> (10 - s). X[p][r] on entry: the folded
@@ -450,11 +580,11 @@ struct NoHook {
 // transform starts (the blind rotation's accumulator): one barrier before
 // the first exchange write.
 template <int P, int NB = kXchgBufs, typename Hook = NoHook, typename Bar = CtaBar,
-          bool kSyncFirst = false>
-__device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
-                                            const double2* __restrict__ tw, uint32_t t, uint32_t tm,
-                                            Hook hook = Hook(), Bar bar = Bar()) {
+          bool kSyncFirst = false, typename TW = const double2*>
+__device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf, TW twsrc, uint32_t t,
+                                            uint32_t tm, Hook hook = Hook(), Bar bar = Bar()) {
   const uint32_t L = t & 31, w = t >> 5;
+  const auto tws = tw_source(twsrc, t);
   // pass A (L_A: regs (x7, x8, x9)): levels 0, 1, 2; every block index is
   // a register index, so the twiddles are constant-bank operands
 #pragma unroll
@@ -475,14 +605,13 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
   // level 4 on x5, block 2 b3 + x6; level 5 on x4, block 4 b3 + (x5, x6)
   const uint32_t u = L >> 1;  // x3..x0
   {
-    const uint32_t b3 = 2 * w + (L & 1);
-    const double2 w3 = twf(tw, 3, b3), w4 = twf(tw, 4, 2 * b3);  // odd level-4 blocks: -i w4
-    double2 w5[2];  // even level-5 blocks 4 b3 + 2 x6; odd ones -i w5
-#pragma unroll
-    for (int q = 0; q < 2; ++q) w5[q] = twf(tw, 5, 4 * b3 + 2 * q);
+    double2 wB[4];  // w3, w4 (odd level-4 blocks: -i w4), w5 of the even level-5 blocks 4 b3 + 2 x6
+    tws.fwdB(wB);
     if constexpr (kSyncFirst) bar.sync();
     xchg_cta<P, NB>(X, buf, bar, [&](int r) { return t + 128u * r; },
                     [&](int r) { return 16u * r + 128u * (L & 1) + u + 256u * w; });
+    tws.ready(wB);
+    const double2 w3 = wB[0], w4 = wB[1], w5[2] = {wB[2], wB[3]};
     probe_mark(3);
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -507,15 +636,12 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
   // x0, x1)): level 6 on x3, block x >> 4 = 16 w + 8 L2 + 4 x6 + 2 L1 + L0;
   // level 7 on x2, block 2 (x >> 4) + x3
   {
-    const uint32_t b6 = 16 * w + 8 * ((L >> 2) & 1) + 2 * ((L >> 1) & 1) + (L & 1);
-    double2 w6[2], w7[2];  // per x6; odd level-7 blocks (x3 = 1): -i w7
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      w6[q] = twf(tw, 6, b6 + 4 * q);
-      w7[q] = twf(tw, 7, 2 * (b6 + 4 * q));
-    }
+    double2 wC[4];  // w6 per x6; w7 per x6 (odd level-7 blocks, x3 = 1: -i w7)
+    tws.fwdC(wC);
     probe_mark(4);
     tm_trip_fwd<P>(X, tm);
+    tws.ready(wC);
+    const double2 w6[2] = {wC[0], wC[1]}, w7[2] = {wC[2], wC[3]};
     probe_mark(5);
     hook();
 #pragma unroll
@@ -534,15 +660,12 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
   // x5, x7)): level 8 on x1, block x >> 2 = 64 w + 32 L4 + 16 x6 + (L & 15);
   // level 9 on x0, block 2 (x >> 2) + x1
   {
-    const uint32_t b8 = 64 * w + 32 * (L >> 4) + (L & 15);
-    double2 w8[2], w9[2];  // per x6; odd level-9 blocks (x1 = 1): -i w9
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      w8[q] = twf(tw, 8, b8 + 16 * q);
-      w9[q] = twf(tw, 9, 2 * (b8 + 16 * q));
-    }
+    double2 wD[4];  // w8 per x6; w9 per x6 (odd level-9 blocks, x1 = 1: -i w9)
+    tws.fwdD(wD);
     probe_mark(6);
     tm_trip_fwd<P>(X, tm);
+    tws.ready(wD);
+    const double2 w8[2] = {wD[0], wD[1]}, w9[2] = {wD[2], wD[3]};
     probe_mark(7);
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -565,11 +688,11 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf,
 // so each thread owns the same accumulator coefficients in both halves of
 // a CMUX. The cross-warp exchange starts with a CTA barrier (other warps
 // may still read buf). The untwist is the caller's.
-template <int P, int NB = kXchgBufs, typename Bar = CtaBar>
-__device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
-                                              const double2* __restrict__ tw, uint32_t t,
-                                              uint32_t tm, Bar bar = Bar()) {
+template <int P, int NB = kXchgBufs, typename Bar = CtaBar, typename TW = const double2*>
+__device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf, TW twsrc,
+                                              uint32_t t, uint32_t tm, Bar bar = Bar()) {
   const uint32_t L = t & 31, w = t >> 5;
+  const auto tws = tw_source(twsrc, t);
   // pass D': stages 9, 8 on (x0, x1) = regs (n0, n1): w in {1, i}
 #pragma unroll
   for (int p = 0; p < P; ++p)
@@ -578,10 +701,12 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
   // L_D -> L_C (TMEM); pass C': stage 7 on x2 = n0 (j = (x0, x1) = L >> 3),
   // stage 6 on x3 = n1 (j = (L >> 3) + 4 x2)
   {
-    const uint32_t j = L >> 3;
-    const double2 v7 = twi(tw, j << 7), v6 = twi(tw, j << 6);  // stage 6, x2 = 1: i v6
+    double2 vC[2];  // v7, v6 (stage 6, x2 = 1: i v6)
+    tws.invC(vC);
     probe_mark(10);
     tm_trip_inv<P>(X, tm);
+    tws.ready(vC);
+    const double2 v7 = vC[0], v6 = vC[1];
     probe_mark(11);
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -599,12 +724,12 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
   // x5 = r1 (j = u + 16 x4), stage 3 on x6 = r2 (j = u + 16 (x4, x5))
   const uint32_t u = L >> 1;
   {
-    const double2 v5 = twi(tw, u << 5), v4 = twi(tw, u << 4);  // stage 4, x4 = 1: i v4
-    double2 v3[2];  // stage 3 per x4; x5 = 1: i v3
-#pragma unroll
-    for (int q = 0; q < 2; ++q) v3[q] = twi(tw, (u << 3) + 128 * q);
+    double2 vB[4];  // v5, v4 (stage 4, x4 = 1: i v4), v3 per x4 (x5 = 1: i v3)
+    tws.invB(vB);
     probe_mark(12);
     tm_trip_inv<P>(X, tm);
+    tws.ready(vB);
+    const double2 v5 = vB[0], v4 = vB[1], v3[2] = {vB[2], vB[3]};
     probe_mark(13);
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -627,14 +752,14 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf,
   }
   // L_B -> L_A (cross-warp); pass A': stage 2 on x7 = r0 (j = t), stage 1
   // on x8 = r1 (j = t + 128 x7), stage 0 on x9 = r2 (j = t + 128 (x7, x8))
-  const double2 v2 = twi(tw, t << 2), v1 = twi(tw, t << 1);  // stage 1, x7 = 1: i v1
-  double2 v0[2];  // stage 0 per x7; x8 = 1: i v0
-#pragma unroll
-  for (int q = 0; q < 2; ++q) v0[q] = twi(tw, t + 128 * q);
+  double2 vA[4];  // v2, v1 (stage 1, x7 = 1: i v1), v0 per x7 (x8 = 1: i v0)
+  tws.invA(vA);
   probe_mark(14);
   bar.sync();
   xchg_cta<P, NB>(X, buf, bar, [&](int r) { return 16u * r + 128u * (L & 1) + u + 256u * w; },
                   [&](int r) { return t + 128u * r; });
+  tws.ready(vA);
+  const double2 v2 = vA[0], v1 = vA[1], v0[2] = {vA[2], vA[3]};
   probe_mark(15);
 #pragma unroll
   for (int p = 0; p < P; ++p)

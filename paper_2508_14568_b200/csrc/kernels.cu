@@ -461,9 +461,14 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
   const uint32_t p = cluster.block_rank();
   __shared__ __align__(8) uint64_t inbox_full[2];  // my inbox buffers' arrival barriers
   __shared__ uint32_t tmem_slot;
-  const uint32_t tmem = tmem_alloc(&tmem_slot, 64);  // up to 2 spectra in lockstep (exact mask CTA)
+  // TMEM: exchange trips for up to 2 spectra in lockstep (exact mask CTA,
+  // columns [0, 64)) + the thread's 22 twiddles (TwTmem, [64, 152))
+  constexpr uint32_t kPairTmemCols = 256;
+  const uint32_t tmem = tmem_alloc(&tmem_slot, kPairTmemCols);
   const uint32_t tm = tmem_warp_base(tmem);
   const uint32_t t = threadIdx.x;
+  const TwTmem twt{tm + 64};
+  twt.fill(TwGlobal{a.twiddles, t});
   // shared::cluster addresses of the partner's inbox and its barriers
   uint32_t r_inbox, r_full;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
@@ -551,7 +556,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
       X[0][r] = make_double2((double)d[0], (double)d[1]);
     }
     probe_mark(1);
-    fft_forward<1, 1>(X, buf, tw, t, tm);
+    fft_forward<1, 1, NoHook, CtaBar, false, TwTmem>(X, buf, twt, t, tm);
     probe_mark(8);
     const uint32_t my_full = (uint32_t)__cvta_generic_to_shared(&inbox_full[parity]);
     if (t == 0)
@@ -601,7 +606,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
           Z[0][q] = mac2(X[0][q], ld_stream(bq), d1, ld_stream(bq + 384));
           Z[1][q] = mac2(X[0][q], ld_stream(bq + 128), d1, ld_stream(bq + 512));
         }
-        fft_inverse_a<2, 1>(Z, buf, tw, t, tm);
+        fft_inverse_a<2, 1, CtaBar, TwTmem>(Z, buf, twt, t, tm);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const double2 ut = make_double2(tz[r].x, -tz[r].y);
@@ -618,7 +623,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
           const double2* bq = bsk + q * (6 * 128);
           X[0][q] = mac2(X[0][q], ld_stream(bq + 640), other_spec[q * 128 + t], ld_stream(bq + 256));
         }
-        fft_inverse_a<1, 1>(X, buf, tw, t, tm);
+        fft_inverse_a<1, 1, CtaBar, TwTmem>(X, buf, twt, t, tm);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const double2 ut = make_double2(tz[r].x, -tz[r].y);
@@ -633,7 +638,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
       continue;
     }
     probe_mark(9);
-    fft_inverse_a<1, 1>(X, buf, tw, t, tm);  // its barriers also order the rotated reads before the update
+    fft_inverse_a<1, 1, CtaBar, TwTmem>(X, buf, twt, t, tm);  // its barriers also order the rotated reads before the update
     probe_mark(16);
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
@@ -667,7 +672,7 @@ __device__ __forceinline__ void blind_rotate_pair_body(const BrArgs& a) {
       atomicAdd(a.done + item / a.done_chunk, 1u);
     }
   }
-  tmem_free(tmem, 64);
+  tmem_free(tmem, kPairTmemCols);
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
