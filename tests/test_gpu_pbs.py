@@ -291,3 +291,32 @@ def test_pbs_bit_exact_throughput_kernel(orc, golden, monkeypatch):
     want = orc.pbs_batch(rows, luts[which])
     assert np.array_equal(got, want)
     c.close()
+
+
+def _host_has_avx512():
+    try:
+        flags = set(open("/proc/cpuinfo").read().split())
+    except OSError:
+        return False
+    return {"avx512f", "avx512dq", "avx512bw", "avx512vl", "fma"} <= flags
+
+
+@pytest.mark.skipif(not _host_has_avx512(), reason="the fast oracle build needs AVX-512")
+def test_cfg2_4096_ciphertexts_bit_exact(ctx):
+    """The whole BASELINE configs[1] batch (4096 cfg2 messages, identity LUT,
+    keys seed 0) through the product path — one throughput-kernel launch
+    over 9+ waves — equals the oracle's PBS word for word on every output
+    LWE (the oracle's lane-vectorised build, itself pinned bit-identical to
+    the scalar checker by tests/test_oracle_pins.py)."""
+    from oracle import oracle as O
+    from paper_2508_14568_b200 import workloads as W
+    o = O.Oracle(0, fast=True)
+    vals = W.cfg2()
+    rows = np.stack([o.encrypt(v, i) for i, v in enumerate(vals)])
+    lid = ctx.lut(L.identity_lut())
+    got = ctx.pbs_host(rows, np.full(len(vals), lid, np.uint32))
+    want = o.pbs_batch_simd(rows, np.tile(np.arange(16, dtype=np.int32), (len(vals), 1)))
+    assert want is not None
+    same = np.all(got == want, axis=1)
+    assert same.all(), f"{int((~same).sum())} of 4096 differ"
+    assert [o.decrypt(r) for r in got[:64]] == vals[:64]
