@@ -43,6 +43,8 @@
 
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace lvb {
@@ -584,6 +586,10 @@ template <int P, int NB = kXchgBufs, typename Hook = NoHook, typename Bar = CtaB
 __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf, TW twsrc, uint32_t t,
                                             uint32_t tm, Hook hook = Hook(), Bar bar = Bar()) {
   const uint32_t L = t & 31, w = t >> 5;
+  // twiddles: the product's throughput kernel loads them from the L1-resident
+  // table inline (TW = const double2*; the pre-policy code, register
+  // allocation unchanged), the latency kernels fetch a pass's set from TMEM
+  constexpr bool kTm = std::is_same<TW, TwTmem>::value;
   const auto tws = tw_source(twsrc, t);
   // pass A (L_A: regs (x7, x8, x9)): levels 0, 1, 2; every block index is
   // a register index, so the twiddles are constant-bank operands
@@ -606,12 +612,26 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf, TW
   const uint32_t u = L >> 1;  // x3..x0
   {
     double2 wB[4];  // w3, w4 (odd level-4 blocks: -i w4), w5 of the even level-5 blocks 4 b3 + 2 x6
-    tws.fwdB(wB);
+    double2 w3, w4, w5[2];
+    if constexpr (kTm) {
+      tws.fwdB(wB);
+    } else {
+      const uint32_t b3 = 2 * w + (L & 1);
+      w3 = twf(twsrc, 3, b3);
+      w4 = twf(twsrc, 4, 2 * b3);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) w5[q] = twf(twsrc, 5, 4 * b3 + 2 * q);
+    }
     if constexpr (kSyncFirst) bar.sync();
     xchg_cta<P, NB>(X, buf, bar, [&](int r) { return t + 128u * r; },
                     [&](int r) { return 16u * r + 128u * (L & 1) + u + 256u * w; });
-    tws.ready(wB);
-    const double2 w3 = wB[0], w4 = wB[1], w5[2] = {wB[2], wB[3]};
+    if constexpr (kTm) {
+      tws.ready(wB);
+      w3 = wB[0];
+      w4 = wB[1];
+      w5[0] = wB[2];
+      w5[1] = wB[3];
+    }
     probe_mark(3);
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -637,11 +657,26 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf, TW
   // level 7 on x2, block 2 (x >> 4) + x3
   {
     double2 wC[4];  // w6 per x6; w7 per x6 (odd level-7 blocks, x3 = 1: -i w7)
-    tws.fwdC(wC);
+    double2 w6[2], w7[2];
+    if constexpr (kTm) {
+      tws.fwdC(wC);
+    } else {
+      const uint32_t b6 = 16 * w + 8 * ((L >> 2) & 1) + 2 * ((L >> 1) & 1) + (L & 1);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        w6[q] = twf(twsrc, 6, b6 + 4 * q);
+        w7[q] = twf(twsrc, 7, 2 * (b6 + 4 * q));
+      }
+    }
     probe_mark(4);
     tm_trip_fwd<P>(X, tm);
-    tws.ready(wC);
-    const double2 w6[2] = {wC[0], wC[1]}, w7[2] = {wC[2], wC[3]};
+    if constexpr (kTm) {
+      tws.ready(wC);
+      w6[0] = wC[0];
+      w6[1] = wC[1];
+      w7[0] = wC[2];
+      w7[1] = wC[3];
+    }
     probe_mark(5);
     hook();
 #pragma unroll
@@ -661,11 +696,26 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf, TW
   // level 9 on x0, block 2 (x >> 2) + x1
   {
     double2 wD[4];  // w8 per x6; w9 per x6 (odd level-9 blocks, x1 = 1: -i w9)
-    tws.fwdD(wD);
+    double2 w8[2], w9[2];
+    if constexpr (kTm) {
+      tws.fwdD(wD);
+    } else {
+      const uint32_t b8 = 64 * w + 32 * (L >> 4) + (L & 15);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        w8[q] = twf(twsrc, 8, b8 + 16 * q);
+        w9[q] = twf(twsrc, 9, 2 * (b8 + 16 * q));
+      }
+    }
     probe_mark(6);
     tm_trip_fwd<P>(X, tm);
-    tws.ready(wD);
-    const double2 w8[2] = {wD[0], wD[1]}, w9[2] = {wD[2], wD[3]};
+    if constexpr (kTm) {
+      tws.ready(wD);
+      w8[0] = wD[0];
+      w8[1] = wD[1];
+      w9[0] = wD[2];
+      w9[1] = wD[3];
+    }
     probe_mark(7);
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -692,6 +742,7 @@ template <int P, int NB = kXchgBufs, typename Bar = CtaBar, typename TW = const 
 __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf, TW twsrc,
                                               uint32_t t, uint32_t tm, Bar bar = Bar()) {
   const uint32_t L = t & 31, w = t >> 5;
+  constexpr bool kTm = std::is_same<TW, TwTmem>::value;
   const auto tws = tw_source(twsrc, t);
   // pass D': stages 9, 8 on (x0, x1) = regs (n0, n1): w in {1, i}
 #pragma unroll
@@ -702,11 +753,21 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf, 
   // stage 6 on x3 = n1 (j = (L >> 3) + 4 x2)
   {
     double2 vC[2];  // v7, v6 (stage 6, x2 = 1: i v6)
-    tws.invC(vC);
+    double2 v7, v6;
+    if constexpr (kTm) {
+      tws.invC(vC);
+    } else {
+      const uint32_t j = L >> 3;
+      v7 = twi(twsrc, j << 7);
+      v6 = twi(twsrc, j << 6);
+    }
     probe_mark(10);
     tm_trip_inv<P>(X, tm);
-    tws.ready(vC);
-    const double2 v7 = vC[0], v6 = vC[1];
+    if constexpr (kTm) {
+      tws.ready(vC);
+      v7 = vC[0];
+      v6 = vC[1];
+    }
     probe_mark(11);
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -725,11 +786,24 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf, 
   const uint32_t u = L >> 1;
   {
     double2 vB[4];  // v5, v4 (stage 4, x4 = 1: i v4), v3 per x4 (x5 = 1: i v3)
-    tws.invB(vB);
+    double2 v5, v4, v3[2];
+    if constexpr (kTm) {
+      tws.invB(vB);
+    } else {
+      v5 = twi(twsrc, u << 5);
+      v4 = twi(twsrc, u << 4);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) v3[q] = twi(twsrc, (u << 3) + 128 * q);
+    }
     probe_mark(12);
     tm_trip_inv<P>(X, tm);
-    tws.ready(vB);
-    const double2 v5 = vB[0], v4 = vB[1], v3[2] = {vB[2], vB[3]};
+    if constexpr (kTm) {
+      tws.ready(vB);
+      v5 = vB[0];
+      v4 = vB[1];
+      v3[0] = vB[2];
+      v3[1] = vB[3];
+    }
     probe_mark(13);
 #pragma unroll
     for (int p = 0; p < P; ++p)
@@ -753,13 +827,26 @@ __device__ __forceinline__ void fft_inverse_a(double2 (&X)[P][8], double2* buf, 
   // L_B -> L_A (cross-warp); pass A': stage 2 on x7 = r0 (j = t), stage 1
   // on x8 = r1 (j = t + 128 x7), stage 0 on x9 = r2 (j = t + 128 (x7, x8))
   double2 vA[4];  // v2, v1 (stage 1, x7 = 1: i v1), v0 per x7 (x8 = 1: i v0)
-  tws.invA(vA);
+  double2 v2, v1, v0[2];
+  if constexpr (kTm) {
+    tws.invA(vA);
+  } else {
+    v2 = twi(twsrc, t << 2);
+    v1 = twi(twsrc, t << 1);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) v0[q] = twi(twsrc, t + 128 * q);
+  }
   probe_mark(14);
   bar.sync();
   xchg_cta<P, NB>(X, buf, bar, [&](int r) { return 16u * r + 128u * (L & 1) + u + 256u * w; },
                   [&](int r) { return t + 128u * r; });
-  tws.ready(vA);
-  const double2 v2 = vA[0], v1 = vA[1], v0[2] = {vA[2], vA[3]};
+  if constexpr (kTm) {
+    tws.ready(vA);
+    v2 = vA[0];
+    v1 = vA[1];
+    v0[0] = vA[2];
+    v0[1] = vA[3];
+  }
   probe_mark(15);
 #pragma unroll
   for (int p = 0; p < P; ++p)
