@@ -576,8 +576,12 @@ __device__ __forceinline__ TwTmem tw_source(TwTmem s, uint32_t) { return s; }
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
-// hook() runs after the first TMEM trip (the caller issues loads it needs
-// right after the transform there, e.g. the first BSK row).
+// hook() issues loads the caller needs right after the transform (the first
+// BSK bin groups): LVB_HOOK_PASS 0 after the first TMEM trip, 1 (default)
+// just before the second, 2 after it (55.86 / 55.55 / 55.56 ms per 4096).
+#ifndef LVB_HOOK_PASS
+#define LVB_HOOK_PASS 1
+#endif
 // kSyncFirst: buf aliases memory other warps may still be reading when the
 // transform starts (the blind rotation's accumulator): one barrier before
 // the first exchange write.
@@ -678,7 +682,9 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf, TW
       w7[1] = wC[3];
     }
     probe_mark(5);
+#if LVB_HOOK_PASS == 0
     hook();
+#endif
 #pragma unroll
     for (int p = 0; p < P; ++p)
 #pragma unroll
@@ -708,7 +714,13 @@ __device__ __forceinline__ void fft_forward(double2 (&X)[P][8], double2* buf, TW
       }
     }
     probe_mark(6);
+#if LVB_HOOK_PASS == 1
+    hook();
+#endif
     tm_trip_fwd<P>(X, tm);
+#if LVB_HOOK_PASS == 2
+    hook();
+#endif
     if constexpr (kTm) {
       tws.ready(wD);
       w8[0] = wD[0];
