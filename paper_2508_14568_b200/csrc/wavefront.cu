@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -54,8 +55,15 @@ static BandSpec to_band(const lv_band* b) {
 // Wave descriptors uploaded per chunk (76 B each: ~160 MB of device memory).
 constexpr size_t kWaveChunkItems = size_t(1) << 21;
 
-// Plan cache bound: ~24 B per cell, so 8M cells is ~200 MB of host memory.
-constexpr uint64_t kPlanCacheCells = 8u << 20;
+// Plan cache bound: ~24 B per cell, so 8M cells is ~200 MB of host memory
+// (LVB_PLAN_CACHE_CELLS overrides it; the tests shrink it to force eviction).
+static uint64_t plan_cache_cells_limit() {
+  static const uint64_t v = [] {
+    const char* e = std::getenv("LVB_PLAN_CACHE_CELLS");
+    return e ? std::strtoull(e, nullptr, 10) : (uint64_t)8 << 20;
+  }();
+  return v;
+}
 
 static std::shared_ptr<const PairPlan> get_plan(lv_ctx* c, uint32_t m, uint32_t n,
                                                 const BandSpec& band, bool negated,
@@ -76,14 +84,14 @@ static std::shared_ptr<const PairPlan> get_plan(lv_ctx* c, uint32_t m, uint32_t 
   auto plan = std::make_shared<const PairPlan>(plan_pair(m, n, band, negated, budget));
   const uint64_t cells = plan->cells.size() + 1;
   // evict least recently used plans until the new one fits
-  while (!c->plan_cache.empty() && c->plan_cache_cells + cells > kPlanCacheCells) {
+  while (!c->plan_cache.empty() && c->plan_cache_cells + cells > plan_cache_cells_limit()) {
     auto lru = c->plan_cache.begin();
     for (auto e = c->plan_cache.begin(); e != c->plan_cache.end(); ++e)
       if (e->second.second < lru->second.second) lru = e;
     c->plan_cache_cells -= lru->second.first->cells.size() + 1;
     c->plan_cache.erase(lru);
   }
-  if (cells <= kPlanCacheCells) {
+  if (cells <= plan_cache_cells_limit()) {
     c->plan_cache.emplace(key, std::make_pair(plan, ++c->plan_cache_tick));
     c->plan_cache_cells += cells;
   }
