@@ -98,3 +98,28 @@ def test_long_pairs(golden):
         for f in ("distance", "half_width", "visited_cells", "pbs_total", "pbs_equality",
                   "pbs_kernel", "refresh_count", "max_key_variance", "linear_ops"):
             assert rep[f] == want[f], (f, rep[f], want[f])
+
+
+def test_eq9_provider_traversal():
+    """kernel::distance with a caller-supplied Eq9Provider (kernel.hpp:162-199,
+    lv_edit_distance_eq9): encrypted 9*[a_i == b_j] handles from the caller,
+    asked once per in-band cell; the distance and the counters match the
+    encrypted-vs-encrypted traversal's kernel part (no equality bootstraps)."""
+    from paper_2508_14568_b200 import leuven as LV
+    ctx = L.Context(seed=21)
+    a, b = "kitten", "sitting"
+    asked = []
+
+    def provider(i, j):
+        asked.append((i, j))
+        return int(ctx.encrypt([9 if a[i - 1] == b[j - 1] else 0])[0])
+    run = LV.distance(ctx, provider, len(a), len(b), LV.BandSpec.exact(len(a), len(b)))
+    assert int(ctx.decrypt([run.score])[0]) == 3
+    assert len(asked) == len(set(asked)) == 42
+    assert (run.kernel_pbs, run.equality_pbs, run.visited_cells) == (42, 0, 42)
+    band = LV.BandSpec.skip(len(a), len(b))
+    asked.clear()
+    run = LV.distance(ctx, provider, len(a), len(b), band)
+    assert int(ctx.decrypt([run.score])[0]) == LV.banded_distance(a, b, band.half_width) % 32
+    assert len(asked) == run.visited_cells < 42
+    ctx.close()
