@@ -174,6 +174,9 @@ __device__ __forceinline__ void own_ld(uint32_t a, int p, int h, uint32_t (&r)[1
       : "memory");
 }
 
+#ifndef LVB_BR_TW_TMEM
+#define LVB_BR_TW_TMEM 0
+#endif
 #ifndef LVB_XCHG_ALIAS
 #define LVB_XCHG_ALIAS 0  // 1: measured 56.1 vs 55.86 ms at 3 CTAs/SM, 57.8 at 4 (profiles/r02_lf_variants.txt)
 #endif
@@ -197,7 +200,10 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
   __shared__ uint32_t tmem_slot;
   // TMEM columns: P spectra x 32 (exchange trips); the throughput kernel also
   // parks its owned accumulator coefficients at [64, 128) (LVB_OWN_TMEM)
-  constexpr uint32_t kTmemCols = kExact ? 128 : (LVB_OWN_TMEM ? 128 : 64);
+  // LVB_BR_TW_TMEM (experiment, with LVB_BR_CTAS=2): the twiddles in TMEM
+  // too ([128, 216) -> 256 columns per CTA)
+  constexpr bool kTwT = LVB_BR_TW_TMEM && !kExact;
+  constexpr uint32_t kTmemCols = kTwT ? 256 : kExact ? 128 : (LVB_OWN_TMEM ? 128 : 64);
   const uint32_t tmem = tmem_alloc(&tmem_slot, kTmemCols);
   const uint32_t tm = tmem_warp_base(tmem);
   const uint32_t t = threadIdx.x;
@@ -218,7 +224,16 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
       acc[kN + j] = s < kN ? tp[s] : (uint64_t)0 - tp[s - kN];
     }
   }
-  const double2* __restrict__ tw = a.twiddles;
+  const double2* __restrict__ tw0 = a.twiddles;
+  const auto tw = [&] {
+    if constexpr (kTwT) {
+      const TwTmem s{tm + 128};
+      s.fill(TwGlobal{tw0, t});
+      return s;
+    } else {
+      return tw0;
+    }
+  }();
   // Thread t owns accumulator coefficients x = t + 128 r (and x + kM) of both
   // polynomials: the forward FFT reads them in that layout and
   // fft_inverse_a returns the external product in it, so each thread
@@ -297,11 +312,11 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         for (int e = 0; e < (kExact ? 6 : 4); ++e)
           bpre[q][e] = ld_stream<true>(bsk_row + (q * (kExact ? 6 : 4) + e) * 128);
     };
-    fft_forward<2, kXchgBufs, decltype(bsk_hook), CtaBar, kAlias>(X, buf, tw, t, tm, bsk_hook);
+    fft_forward<2, kXchgBufs, decltype(bsk_hook), CtaBar, kAlias, std::remove_const_t<decltype(tw)>>(X, buf, tw, t, tm, bsk_hook);
     probe_mark(8);
 #define BSK_AT(q, e, ptr) ((q) < kEarly ? bpre[(q) < kEarly ? (q) : 0][e] : ld_stream<true>(ptr))
 #else
-    fft_forward<2, kXchgBufs, NoHook, CtaBar, kAlias>(X, buf, tw, t, tm);
+    fft_forward<2, kXchgBufs, NoHook, CtaBar, kAlias, std::remove_const_t<decltype(tw)>>(X, buf, tw, t, tm);
 #define BSK_AT(q, e, ptr) ld_stream<true>(ptr)
 #endif
 
@@ -325,7 +340,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         Z[1][q] = mac2(d0, l0, d1, l1);
         Z[2][q] = mac2(d1, b1, d0, b0);  // body output: row 1 first
       }
-      fft_inverse_a<3>(Z, buf, tw, t, tm);
+      fft_inverse_a<3>(Z, buf, tw0, t, tm);
       if constexpr (kAlias) __syncthreads();  // every warp's exchange reads precede the update
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
@@ -355,7 +370,7 @@ __device__ __forceinline__ void blind_rotate_body(const BrArgs& a) {
         X[1][q] = mac2(d1, b11, d0, b01);  // output o: row o first
       }
       probe_mark(9);
-      fft_inverse_a<2>(X, buf, tw, t, tm);
+      fft_inverse_a<2, kXchgBufs, CtaBar, std::remove_const_t<decltype(tw)>>(X, buf, tw, t, tm);
       probe_mark(16);
       if constexpr (kAlias) __syncthreads();  // every warp's exchange reads precede the update
 #if LVB_OWN_TMEM
